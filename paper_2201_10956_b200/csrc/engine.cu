@@ -1,0 +1,822 @@
+// engine.cu — sm_100a kernels and the device half of the C ABI (include/epi3cu.h).
+//
+// The hot path of the reference (run_search, /root/reference/proj/src/search.cpp:127-250
+// with blocked_pass/accumulate_reduced, src/kernels.cpp:30-53, 236-324, and
+// k2_score, src/scoring.cpp:23-35) redesigned for B200:
+//
+//  * Device layout. Per class c, planes are stored word-quad-major:
+//      planes[c][wq][snp][g]  (uint4 = 128 samples, g in {0,1})
+//    so the 32 lanes of a warp, which own 32 consecutive SNPs k, read one
+//    contiguous 1 KiB per word-quad (fully coalesced 128-bit loads), while
+//    the SNPs a warp shares (i, j) are warp-uniform broadcast loads.
+//    Genotype 2 is never stored (bitplane.hpp:13-20) — and never computed.
+//
+//  * Marginal-subtraction contingency tables. Per triple and 32-sample word
+//    only the 8 cells with genotypes in {0,1}^3 are counted (8 LOP3-AND +
+//    8 POPC); the other 19 cells per class follow exactly, in u32
+//    arithmetic, from the per-dataset marginal index (pair counts of planes
+//    {0,1}x{0,1} for every SNP pair, single plane counts) and N_c. This is
+//    bit-identical to the 27-POPC NOR formulation (kernels.cpp:38-49) and
+//    needs neither plane 2 nor the padding mask (padding bits are zero in
+//    planes 0/1, so they never count).
+//
+//  * Blocked i<j<k enumeration. A CTA work item is (i, j-tile, k-tile) of
+//    32x32 triples in the (j,k) triangle above i; warp w owns j = tile+w+8q
+//    (q<4), lane l owns k = tile+l. Items are linearised i-major so any
+//    lexicographic triple-rank range maps to one contiguous item range
+//    (boundary lanes masked by rank) — the unit of the multi-GPU partition.
+//    Persistent CTAs take equal contiguous item slices.
+//
+//  * Fused K2 + top-k. The K2 epilogue uses the host-built log table
+//    (build_log_table, scoring.cpp:14-21) with the reference's exact fp64
+//    grouping and row order; candidates go to a per-warp sorted top-k list
+//    in shared memory ordered exactly like hit_less (search.hpp:29-35), with
+//    a global monotone threshold shared through atomicMin. A bitonic merge
+//    kernel reduces the per-warp lists to the final top-k.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "epi3cu.h"
+#include "internal.h"
+
+using e3::fail;
+
+namespace {
+
+constexpr int kTile = 32;                  // j / k tile edge (one SNP per lane)
+constexpr int kWarps = 8;                  // warps per search CTA
+constexpr int kJPerWarp = kTile / kWarps;  // 4 j's per warp -> 4 triples per lane
+constexpr int kMergeCap = 4096;            // entries per bitonic merge CTA
+constexpr uint32_t kMaxSnps = (1u << 21) - 1;
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t err__ = (expr);                                                     \
+    if (err__ != cudaSuccess)                                                       \
+      return fail(err__ == cudaErrorMemoryAllocation ? E3_OOM : E3_CUDA,            \
+                  std::string(#expr) + ": " + cudaGetErrorString(err__));           \
+  } while (0)
+
+// ------------------------------------------------------------------------
+// Order-preserving keys: (score key, triple key) compared as a 128-bit
+// integer is exactly hit_less (search.hpp:29-35).
+// ------------------------------------------------------------------------
+__host__ __device__ inline uint64_t score_key(double s) {
+  if (s == 0.0) s = 0.0;  // fold -0.0
+  uint64_t b;
+  memcpy(&b, &s, 8);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double key_score(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double s;
+  memcpy(&s, &b, 8);
+  return s;
+}
+__host__ __device__ inline uint64_t triple_key(uint32_t i, uint32_t j, uint32_t k) {
+  return (uint64_t(i) << 42) | (uint64_t(j) << 21) | uint64_t(k);
+}
+__device__ __forceinline__ bool key_less(uint64_t as, uint64_t at, uint64_t bs, uint64_t bt) {
+  return as < bs || (as == bs && at < bt);
+}
+
+struct DevData {
+  uint32_t M;
+  uint32_t wq[2];            // uint4 word-quads per class
+  uint32_t n[2];             // class sample counts N0, N1
+  const uint4* planes[2];    // [wq][M][2]
+  const uint2* single[2];    // [M]: popc(plane0), popc(plane1)
+  const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y)
+  const double* logp;        // build_log_table(N+1): N+2 entries
+  const uint64_t* itemoff;   // [M-1] prefix item counts per i
+};
+
+// ------------------------------------------------------------------------
+// The 27-cell table of one class from the 8 counted cells and the marginals.
+// T[a*4+b*2+g] = #samples with genotypes (a,b,g), a,b,g in {0,1}, for SNPs
+// (i,j,k). Output cells in reference order gx*9+gy*3+gz (scoring.hpp:14-16).
+// All arithmetic is exact modulo 2^32 and every result is a true count.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void derive_cells(const uint32_t* T, uint4 pij, uint4 pik, uint4 pjk,
+                                             uint2 si, uint2 sj, uint2 sk, uint32_t N,
+                                             uint32_t* n) {
+  const uint32_t Pij[2][2] = {{pij.x, pij.y}, {pij.z, pij.w}};
+  const uint32_t Pik[2][2] = {{pik.x, pik.y}, {pik.z, pik.w}};
+  const uint32_t Pjk[2][2] = {{pjk.x, pjk.y}, {pjk.z, pjk.w}};
+  const uint32_t Si[2] = {si.x, si.y}, Sj[2] = {sj.x, sj.y}, Sk[2] = {sk.x, sk.y};
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) n[a * 9 + b * 3 + g] = T[a * 4 + b * 2 + g];
+      n[a * 9 + b * 3 + 2] = Pij[a][b] - T[a * 4 + b * 2] - T[a * 4 + b * 2 + 1];
+    }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int g = 0; g < 2; ++g) n[a * 9 + 6 + g] = Pik[a][g] - T[a * 4 + g] - T[a * 4 + 2 + g];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int g = 0; g < 2; ++g) n[18 + b * 3 + g] = Pjk[b][g] - T[b * 2 + g] - T[4 + b * 2 + g];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+    n[a * 9 + 8] = Si[a] - Pij[a][0] - Pij[a][1] - n[a * 9 + 6] - n[a * 9 + 7];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+    n[18 + b * 3 + 2] = Sj[b] - Pij[0][b] - Pij[1][b] - n[18 + b * 3] - n[18 + b * 3 + 1];
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+    n[24 + g] = Sk[g] - Pik[0][g] - Pik[1][g] - n[18 + g] - n[21 + g];
+  const uint32_t n2xx = N - Si[0] - Si[1];
+  const uint32_t n20x = Sj[0] - Pij[0][0] - Pij[1][0];
+  const uint32_t n21x = Sj[1] - Pij[0][1] - Pij[1][1];
+  n[26] = n2xx - n20x - n21x - n[24] - n[25];
+}
+
+// k2_score (scoring.cpp:23-35): identical grouping and row order; explicit
+// round-to-nearest adds so no contraction or reassociation can occur.
+__device__ __forceinline__ double k2_device(const uint32_t* n0, const uint32_t* n1,
+                                            const double* __restrict__ P) {
+  double score = 0.0;
+#pragma unroll
+  for (int c = 0; c < 27; ++c) {
+    const uint32_t r0 = n0[c], r1 = n1[c];
+    const double t = __dadd_rn(__ldg(P + r0), __ldg(P + r1));
+    score = __dadd_rn(score, __dsub_rn(__ldg(P + (size_t(r0) + r1 + 1)), t));
+  }
+  return score;
+}
+
+// One 32-sample word of one class for one (i, j, k): 8 AND3 + 8 POPC.
+__device__ __forceinline__ void count_word(uint32_t xi0, uint32_t xi1, uint32_t xj0, uint32_t xj1,
+                                           uint32_t xk0, uint32_t xk1, uint32_t* T) {
+  T[0] += __popc(xi0 & xj0 & xk0);
+  T[1] += __popc(xi0 & xj0 & xk1);
+  T[2] += __popc(xi0 & xj1 & xk0);
+  T[3] += __popc(xi0 & xj1 & xk1);
+  T[4] += __popc(xi1 & xj0 & xk0);
+  T[5] += __popc(xi1 & xj0 & xk1);
+  T[6] += __popc(xi1 & xj1 & xk0);
+  T[7] += __popc(xi1 & xj1 & xk1);
+}
+
+__device__ __forceinline__ void count_quad(const uint4& i0, const uint4& i1, const uint4& j0,
+                                           const uint4& j1, const uint4& k0, const uint4& k1,
+                                           uint32_t* T) {
+  count_word(i0.x, i1.x, j0.x, j1.x, k0.x, k1.x, T);
+  count_word(i0.y, i1.y, j0.y, j1.y, k0.y, k1.y, T);
+  count_word(i0.z, i1.z, j0.z, j1.z, k0.z, k1.z, T);
+  count_word(i0.w, i1.w, j0.w, j1.w, k0.w, k1.w, T);
+}
+
+// Accumulates one class of the CTA item into T[q][8] for this lane.
+__device__ __forceinline__ void accumulate_class(const uint4* __restrict__ planes, uint32_t wq,
+                                                 uint32_t M, uint32_t i, const uint32_t* jc,
+                                                 uint32_t kc, uint32_t (&T)[kJPerWarp][8]) {
+#pragma unroll
+  for (int q = 0; q < kJPerWarp; ++q)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) T[q][c] = 0;
+  const size_t row = size_t(M) * 2;
+  const uint4* p = planes;
+#pragma unroll 1
+  for (uint32_t w = 0; w < wq; ++w, p += row) {
+    const uint4 i0 = __ldg(p + 2 * i), i1 = __ldg(p + 2 * i + 1);
+    const uint4 k0 = __ldg(p + 2 * kc), k1 = __ldg(p + 2 * kc + 1);
+#pragma unroll
+    for (int q = 0; q < kJPerWarp; ++q) {
+      const uint4 j0 = __ldg(p + 2 * jc[q]), j1 = __ldg(p + 2 * jc[q] + 1);
+      count_quad(i0, i1, j0, j1, k0, k1, T[q]);
+    }
+  }
+}
+
+struct SearchArgs {
+  uint64_t item_begin, item_count;
+  uint64_t rank_begin, rank_end;  // used when ranged
+  uint32_t top_k;
+  uint64_t* gthr;                 // global score-key threshold
+  ulonglong2* out_lists;          // [gridDim*kWarps][top_k] (skey, tkey)
+  uint32_t* out_counts;           // [gridDim*kWarps]
+};
+
+__device__ __forceinline__ uint32_t tiles_of(uint32_t M, uint32_t i) {
+  return (M - 1 - i + kTile - 1) / kTile;
+}
+
+// Warp-cooperative ordered insert into this warp's shared-memory list.
+__device__ void warp_insert(uint64_t* ls, uint64_t* lt, uint32_t& n, uint32_t K, unsigned cand,
+                            uint64_t s, uint64_t t, int lane, uint64_t* gthr) {
+  while (cand) {
+    const int src = __ffs(cand) - 1;
+    cand &= cand - 1;
+    const uint64_t cs = __shfl_sync(0xffffffffu, s, src);
+    const uint64_t ct = __shfl_sync(0xffffffffu, t, src);
+    if (n == K && !key_less(cs, ct, ls[K - 1], lt[K - 1])) continue;
+    uint32_t cnt = 0;
+    for (uint32_t e = lane; e < n; e += 32) cnt += key_less(ls[e], lt[e], cs, ct);
+    const uint32_t p = __reduce_add_sync(0xffffffffu, cnt);
+    const uint32_t last = (n == K) ? K - 1 : n;  // [p, last) moves to [p+1, last+1)
+    for (int base = int(last) - 1; base >= int(p); base -= 32) {
+      const int e = base - lane;
+      uint64_t vs = 0, vt = 0;
+      if (e >= int(p)) { vs = ls[e]; vt = lt[e]; }
+      __syncwarp();
+      if (e >= int(p)) { ls[e + 1] = vs; lt[e + 1] = vt; }
+      __syncwarp();
+    }
+    if (lane == 0) { ls[p] = cs; lt[p] = ct; }
+    __syncwarp();
+    if (n < K) ++n;
+    if (n == K && lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(gthr),
+                                       (unsigned long long)ls[K - 1]);
+  }
+}
+
+template <bool kRanged>
+__global__ void __launch_bounds__(kWarps * 32, 2)
+search_kernel(const DevData d, const SearchArgs a) {
+  extern __shared__ uint64_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t K = a.top_k;
+  uint64_t* ls = smem + size_t(warp) * 2 * K;
+  uint64_t* lt = ls + K;
+  uint32_t n = 0;
+  const uint32_t M = d.M;
+
+  uint64_t it = a.item_begin + a.item_count * blockIdx.x / gridDim.x;
+  const uint64_t it_end = a.item_begin + a.item_count * (blockIdx.x + 1) / gridDim.x;
+  uint32_t i = 0, ta = 0, tb = 0, nt = 0;
+  if (it < it_end) {
+    // decode: i by binary search over itemoff, then (ta, tb) in the tile triangle
+    uint32_t lo = 0, hi = M - 3;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (d.itemoff[mid] <= it) lo = mid; else hi = mid - 1;
+    }
+    i = lo;
+    nt = tiles_of(M, i);
+    const uint64_t u = it - d.itemoff[i];
+    uint32_t alo = 0, ahi = nt - 1;
+    while (alo < ahi) {
+      const uint32_t mid = (alo + ahi + 1) >> 1;
+      const uint64_t cum = uint64_t(mid) * nt - uint64_t(mid) * (mid - 1) / 2;
+      if (cum <= u) alo = mid; else ahi = mid - 1;
+    }
+    ta = alo;
+    tb = ta + uint32_t(u - (uint64_t(ta) * nt - uint64_t(ta) * (ta - 1) / 2));
+  }
+
+  for (; it < it_end; ++it) {
+    const uint32_t jbase = i + 1 + ta * kTile, kbase = i + 1 + tb * kTile;
+    const uint32_t k = kbase + lane;
+    const uint32_t kc = min(k, M - 1);
+    uint32_t j[kJPerWarp], jc[kJPerWarp];
+#pragma unroll
+    for (int q = 0; q < kJPerWarp; ++q) {
+      j[q] = jbase + warp + kWarps * q;
+      jc[q] = min(j[q], M - 1);
+    }
+    uint32_t T0[kJPerWarp][8], T1[kJPerWarp][8];
+    accumulate_class(d.planes[0], d.wq[0], M, i, jc, kc, T0);
+    accumulate_class(d.planes[1], d.wq[1], M, i, jc, kc, T1);
+
+    const uint64_t gth = *reinterpret_cast<volatile uint64_t*>(a.gthr);
+    uint64_t rank_ij = 0;
+    if (kRanged) {
+      // rank(i, j, k) = C(M,3) - C(M-i,3) + C(M-1-i,2) - C(M-j,2) + (k-j-1)
+      const uint64_t Mi = M - i;
+      rank_ij = (uint64_t(M) * (M - 1) * (M - 2) - Mi * (Mi - 1) * (Mi - 2)) / 6 +
+                (uint64_t(Mi - 1) * (Mi - 2)) / 2;
+    }
+    const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
+    const uint2 sk0 = __ldg(d.single[0] + kc), sk1 = __ldg(d.single[1] + kc);
+    const uint4 pik0 = __ldg(d.pair[0] + size_t(i) * M + kc);
+    const uint4 pik1 = __ldg(d.pair[1] + size_t(i) * M + kc);
+#pragma unroll
+    for (int q = 0; q < kJPerWarp; ++q) {
+      bool valid = j[q] < k && k < M;
+      if (kRanged && valid) {
+        const uint64_t Mj = M - j[q];
+        const uint64_t r = rank_ij - Mj * (Mj - 1) / 2 + (k - j[q] - 1);
+        valid = r >= a.rank_begin && r < a.rank_end;
+      }
+      uint64_t s = ~0ull, t = ~0ull;
+      if (valid) {
+        uint32_t n0[27], n1[27];
+        derive_cells(T0[q], __ldg(d.pair[0] + size_t(i) * M + jc[q]), pik0,
+                     __ldg(d.pair[0] + size_t(jc[q]) * M + kc), si0,
+                     __ldg(d.single[0] + jc[q]), sk0, d.n[0], n0);
+        derive_cells(T1[q], __ldg(d.pair[1] + size_t(i) * M + jc[q]), pik1,
+                     __ldg(d.pair[1] + size_t(jc[q]) * M + kc), si1,
+                     __ldg(d.single[1] + jc[q]), sk1, d.n[1], n1);
+        s = score_key(k2_device(n0, n1, d.logp));
+        t = triple_key(i, j[q], k);
+      }
+      const bool want = valid && s <= gth && (n < K || key_less(s, t, ls[K - 1], lt[K - 1]));
+      const unsigned cand = __ballot_sync(0xffffffffu, want);
+      if (cand) warp_insert(ls, lt, n, K, cand, s, t, lane, a.gthr);
+    }
+
+    // advance to the next item in (i, ta, tb) order
+    if (++tb == nt) {
+      if (++ta == nt) {
+        ++i;
+        ta = 0;
+        nt = tiles_of(M, i);
+      }
+      tb = ta;
+    }
+  }
+
+  const size_t list = size_t(blockIdx.x) * kWarps + warp;
+  for (uint32_t e = lane; e < n; e += 32) a.out_lists[list * K + e] = make_ulonglong2(ls[e], lt[e]);
+  if (lane == 0) a.out_counts[list] = n;
+}
+
+// Bitonic merge of `group` consecutive lists (each <= K sorted entries) into
+// one list of the K smallest entries under hit_less order.
+__global__ void __launch_bounds__(1024) merge_kernel(const ulonglong2* __restrict__ in,
+                                                     const uint32_t* __restrict__ in_counts,
+                                                     uint32_t nlists, uint32_t K, uint32_t group,
+                                                     uint32_t P, ulonglong2* out,
+                                                     uint32_t* out_counts) {
+  extern __shared__ ulonglong2 buf[];
+  const uint32_t first = blockIdx.x * group;
+  const uint32_t last = min(first + group, nlists);
+  for (uint32_t x = threadIdx.x; x < P; x += blockDim.x) {
+    const uint32_t l = first + x / K, e = x % K;
+    ulonglong2 v = make_ulonglong2(~0ull, ~0ull);
+    if (l < last && x < group * K && e < in_counts[l]) v = in[size_t(l) * K + e];
+    buf[x] = v;
+  }
+  __syncthreads();
+  for (uint32_t size = 2; size <= P; size <<= 1)
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t t = threadIdx.x; t < P / 2; t += blockDim.x) {
+        const uint32_t lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const ulonglong2 x = buf[lo], y = buf[hi];
+        const bool gt = key_less(y.x, y.y, x.x, x.y);
+        if (gt == asc) { buf[lo] = y; buf[hi] = x; }
+      }
+      __syncthreads();
+    }
+  uint32_t cnt = 0;
+  for (uint32_t x = threadIdx.x; x < K; x += blockDim.x) {
+    out[size_t(blockIdx.x) * K + x] = buf[x];
+  }
+  if (threadIdx.x == 0) {
+    while (cnt < K && cnt < P && buf[cnt].x != ~0ull) ++cnt;
+    out_counts[blockIdx.x] = cnt;
+  }
+}
+
+// ------------------------------------------------------------------------
+// Dataset preparation kernels
+// ------------------------------------------------------------------------
+// raw: BitPlaneDataset::data_[c] on device, [M][2][W64]; out: [wq][M][2] uint4.
+// Also checks plane exclusivity and clean padding (bitplane.hpp:16-20).
+__global__ void repack_kernel(const uint64_t* __restrict__ raw, uint32_t M, uint32_t w64,
+                              uint32_t wq, uint64_t tail_mask, uint4* __restrict__ out,
+                              uint32_t* bad) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= uint64_t(wq) * M) return;
+  const uint32_t q = uint32_t(t / M), snp = uint32_t(t % M);
+  uint64_t w[2][2];
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t x = 2 * q + h;
+      w[g][h] = x < w64 ? raw[(size_t(snp) * 2 + g) * w64 + x] : 0ull;
+    }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t x = 2 * q + h;
+    if (x < w64) {
+      uint64_t viol = w[0][h] & w[1][h];
+      if (x + 1 == w64) viol |= (w[0][h] | w[1][h]) & ~tail_mask;
+      if (viol) atomicOr(bad, 1u);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+    out[(size_t(q) * M + snp) * 2 + g] =
+        make_uint4(uint32_t(w[g][0]), uint32_t(w[g][0] >> 32), uint32_t(w[g][1]),
+                   uint32_t(w[g][1] >> 32));
+}
+
+__global__ void singles_kernel(const uint4* __restrict__ planes, uint32_t M, uint32_t wq,
+                               uint2* __restrict__ single) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= M) return;
+  uint32_t s0 = 0, s1 = 0;
+  for (uint32_t w = 0; w < wq; ++w) {
+    const uint4 a = planes[(size_t(w) * M + x) * 2], b = planes[(size_t(w) * M + x) * 2 + 1];
+    s0 += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+    s1 += __popc(b.x) + __popc(b.y) + __popc(b.z) + __popc(b.w);
+  }
+  single[x] = make_uint2(s0, s1);
+}
+
+// pair[x*M + y] for x < y: {popc(X0x&X0y), popc(X0x&X1y), popc(X1x&X0y), popc(X1x&X1y)}.
+__global__ void pairs_kernel(const uint4* __restrict__ planes, uint32_t M, uint32_t wq,
+                             uint4* __restrict__ pair) {
+  const uint32_t x = blockIdx.y;
+  const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x * blockDim.x + blockDim.x <= x + 1) return;  // whole block below diagonal
+  const uint32_t yc = min(y, M - 1);
+  uint32_t c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+  const size_t row = size_t(M) * 2;
+  const uint4* p = planes;
+  for (uint32_t w = 0; w < wq; ++w, p += row) {
+    const uint4 x0 = __ldg(p + 2 * x), x1 = __ldg(p + 2 * x + 1);
+    const uint4 y0 = __ldg(p + 2 * yc), y1 = __ldg(p + 2 * yc + 1);
+    c00 += __popc(x0.x & y0.x) + __popc(x0.y & y0.y) + __popc(x0.z & y0.z) + __popc(x0.w & y0.w);
+    c01 += __popc(x0.x & y1.x) + __popc(x0.y & y1.y) + __popc(x0.z & y1.z) + __popc(x0.w & y1.w);
+    c10 += __popc(x1.x & y0.x) + __popc(x1.y & y0.y) + __popc(x1.z & y0.z) + __popc(x1.w & y0.w);
+    c11 += __popc(x1.x & y1.x) + __popc(x1.y & y1.y) + __popc(x1.z & y1.z) + __popc(x1.w & y1.w);
+  }
+  if (y > x && y < M) pair[size_t(x) * M + y] = make_uint4(c00, c01, c10, c11);
+}
+
+// Per-triple tables / scores through the same marginal derivation as the search.
+__global__ void triples_kernel(const DevData d, const uint32_t* __restrict__ triples, uint64_t n,
+                               uint32_t* __restrict__ tables, double* __restrict__ scores) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t i = triples[3 * t], j = triples[3 * t + 1], k = triples[3 * t + 2];
+  const uint32_t M = d.M;
+  uint32_t cells[2][27];
+  for (int c = 0; c < 2; ++c) {
+    uint32_t T[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint4* p = d.planes[c];
+    for (uint32_t w = 0; w < d.wq[c]; ++w, p += size_t(M) * 2)
+      count_quad(p[2 * i], p[2 * i + 1], p[2 * j], p[2 * j + 1], p[2 * k], p[2 * k + 1], T);
+    derive_cells(T, d.pair[c][size_t(i) * M + j], d.pair[c][size_t(i) * M + k],
+                 d.pair[c][size_t(j) * M + k], d.single[c][i], d.single[c][j], d.single[c][k],
+                 d.n[c], cells[c]);
+  }
+  if (tables)
+    for (int c = 0; c < 2; ++c)
+      for (int x = 0; x < 27; ++x) tables[54 * t + 27 * c + x] = cells[c][x];
+  if (scores) scores[t] = k2_device(cells[0], cells[1], d.logp);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI: dataset lifetime
+// ---------------------------------------------------------------------------
+struct e3_dataset {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t M = 0, N[2] = {0, 0};
+  uint32_t wq[2] = {0, 0};
+  uint4* planes[2] = {nullptr, nullptr};
+  uint2* single[2] = {nullptr, nullptr};
+  uint4* pair[2] = {nullptr, nullptr};
+  double* logp = nullptr;
+  uint64_t* itemoff = nullptr;
+  std::vector<uint64_t> h_itemoff;
+  int num_sms = 0, search_ctas_per_sm = 0;
+  // scratch reused across searches
+  ulonglong2* lists[2] = {nullptr, nullptr};
+  uint32_t* counts[2] = {nullptr, nullptr};
+  size_t lists_cap = 0;
+  uint64_t* gthr = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+void release(e3_dataset* ds) {
+  if (!ds) return;
+  cudaSetDevice(ds->device);
+  for (int c = 0; c < 2; ++c) {
+    cudaFree(ds->planes[c]);
+    cudaFree(ds->single[c]);
+    cudaFree(ds->pair[c]);
+    cudaFree(ds->lists[c]);
+    cudaFree(ds->counts[c]);
+  }
+  cudaFree(ds->logp);
+  cudaFree(ds->itemoff);
+  cudaFree(ds->gthr);
+  for (auto& e : ds->ev)
+    if (e) cudaEventDestroy(e);
+  if (ds->stream) cudaStreamDestroy(ds->stream);
+  delete ds;
+}
+
+DevData dev_view(const e3_dataset* ds) {
+  DevData d;
+  d.M = uint32_t(ds->M);
+  for (int c = 0; c < 2; ++c) {
+    d.wq[c] = ds->wq[c];
+    d.n[c] = uint32_t(ds->N[c]);
+    d.planes[c] = ds->planes[c];
+    d.single[c] = ds->single[c];
+    d.pair[c] = ds->pair[c];
+  }
+  d.logp = ds->logp;
+  d.itemoff = ds->itemoff;
+  return d;
+}
+
+int build(e3_dataset* ds, const uint64_t* host[2]) {
+  CUDA_TRY(cudaSetDevice(ds->device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+  for (auto& e : ds->ev) CUDA_TRY(cudaEventCreate(&e));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, ds->device));
+  ds->num_sms = prop.multiProcessorCount;
+  const uint32_t M = uint32_t(ds->M);
+  uint32_t* bad = nullptr;
+  CUDA_TRY(cudaMalloc(&bad, sizeof(uint32_t)));
+  CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), ds->stream));
+  for (int c = 0; c < 2; ++c) {
+    const uint64_t n = ds->N[c];
+    const uint32_t w64 = uint32_t((n + 63) / 64);
+    ds->wq[c] = uint32_t((n + 127) / 128);
+    CUDA_TRY(cudaMalloc(&ds->single[c], sizeof(uint2) * M));
+    CUDA_TRY(cudaMalloc(&ds->pair[c], sizeof(uint4) * size_t(M) * M));
+    CUDA_TRY(cudaMalloc(&ds->planes[c], sizeof(uint4) * std::max<size_t>(1, size_t(ds->wq[c]) * M * 2)));
+    if (ds->wq[c] == 0) {
+      CUDA_TRY(cudaMemsetAsync(ds->single[c], 0, sizeof(uint2) * M, ds->stream));
+      CUDA_TRY(cudaMemsetAsync(ds->pair[c], 0, sizeof(uint4) * size_t(M) * M, ds->stream));
+      continue;
+    }
+    uint64_t* raw = nullptr;
+    const size_t raw_bytes = sizeof(uint64_t) * size_t(M) * 2 * w64;
+    CUDA_TRY(cudaMalloc(&raw, raw_bytes));
+    CUDA_TRY(cudaMemcpyAsync(raw, host[c], raw_bytes, cudaMemcpyHostToDevice, ds->stream));
+    const uint64_t rem = n % 64;
+    const uint64_t tail = rem == 0 ? ~0ull : ((1ull << rem) - 1);
+    const uint64_t threads = uint64_t(ds->wq[c]) * M;
+    repack_kernel<<<unsigned((threads + 255) / 256), 256, 0, ds->stream>>>(
+        raw, M, w64, ds->wq[c], tail, ds->planes[c], bad);
+    singles_kernel<<<(M + 255) / 256, 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
+                                                          ds->single[c]);
+    pairs_kernel<<<dim3((M + 255) / 256, M), 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
+                                                                 ds->pair[c]);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(ds->stream));
+    CUDA_TRY(cudaFree(raw));
+  }
+  // K2 log table, built on the host exactly like build_log_table(N+1).
+  const uint64_t N = ds->N[0] + ds->N[1];
+  std::vector<double> logp(N + 2);
+  e3_build_log_table(N + 1, logp.data());
+  CUDA_TRY(cudaMalloc(&ds->logp, sizeof(double) * logp.size()));
+  CUDA_TRY(cudaMemcpyAsync(ds->logp, logp.data(), sizeof(double) * logp.size(),
+                           cudaMemcpyHostToDevice, ds->stream));
+  // Item prefix over i (items = 32x32 (j,k) tiles above i, i-major).
+  ds->h_itemoff.assign(M - 1, 0);
+  for (uint32_t i = 0; i + 2 < M; ++i) {
+    const uint64_t nt = (M - 1 - i + kTile - 1) / kTile;
+    ds->h_itemoff[i + 1] = ds->h_itemoff[i] + nt * (nt + 1) / 2;
+  }
+  CUDA_TRY(cudaMalloc(&ds->itemoff, sizeof(uint64_t) * ds->h_itemoff.size()));
+  CUDA_TRY(cudaMemcpyAsync(ds->itemoff, ds->h_itemoff.data(),
+                           sizeof(uint64_t) * ds->h_itemoff.size(), cudaMemcpyHostToDevice,
+                           ds->stream));
+  CUDA_TRY(cudaMalloc(&ds->gthr, sizeof(uint64_t)));
+  uint32_t h_bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
+  CUDA_TRY(cudaStreamSynchronize(ds->stream));
+  CUDA_TRY(cudaFree(bad));
+  if (h_bad)
+    return fail(E3_DOMAIN,
+                "bit planes violate the dataset invariants (overlapping genotype planes or "
+                "set padding bits)");
+  CUDA_TRY(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(ulonglong2) * 2 * kMergeCap)));
+  CUDA_TRY(cudaFuncSetAttribute(search_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K)));
+  CUDA_TRY(cudaFuncSetAttribute(search_kernel<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K)));
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, search_kernel<false>, kWarps * 32, 2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K));
+  ds->search_ctas_per_sm = std::max(1, occ);
+  return E3_OK;
+}
+
+}  // namespace
+
+extern "C" int e3_device_count(int* count) {
+  CUDA_TRY(cudaGetDeviceCount(count));
+  return E3_OK;
+}
+
+extern "C" int e3_dataset_create(uint64_t M, uint64_t N0, uint64_t N1, const uint64_t* ctrl,
+                                 const uint64_t* cases, int device, e3_dataset** out) {
+  *out = nullptr;
+  if (M < 3) return fail(E3_DIMENSION, "search needs at least 3 SNPs");
+  if (M > kMaxSnps) return fail(E3_DOMAIN, "at most 2^21-1 SNPs are supported");
+  if (N0 + N1 == 0) return fail(E3_DIMENSION, "dataset has no samples");
+  if (N0 > 0xffffffffull || N1 > 0xffffffffull)
+    return fail(E3_DOMAIN, "class sample count exceeds the 32-bit cell cap");
+  if ((N0 && !ctrl) || (N1 && !cases)) return fail(E3_DOMAIN, "missing plane data");
+  e3_dataset* ds = new e3_dataset;
+  ds->device = device;
+  ds->M = M;
+  ds->N[0] = N0;
+  ds->N[1] = N1;
+  const uint64_t* host[2] = {ctrl, cases};
+  if (int rc = build(ds, host)) {
+    release(ds);
+    return rc;
+  }
+  *out = ds;
+  return E3_OK;
+}
+
+extern "C" void e3_dataset_destroy(e3_dataset* ds) { release(ds); }
+
+extern "C" int e3_dataset_info(const e3_dataset* ds, uint64_t* M, uint64_t* N0, uint64_t* N1,
+                               int* device) {
+  if (!ds) return fail(E3_DOMAIN, "null dataset");
+  if (M) *M = ds->M;
+  if (N0) *N0 = ds->N[0];
+  if (N1) *N1 = ds->N[1];
+  if (device) *device = ds->device;
+  return E3_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI: search
+// ---------------------------------------------------------------------------
+extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit* top,
+                         uint32_t* n_top, e3_stats* stats) {
+  const auto t_start = std::chrono::steady_clock::now();
+  e3_dataset* ds = const_cast<e3_dataset*>(cds);
+  if (!ds) return fail(E3_DOMAIN, "null dataset");
+  if (cfg->top_k < 1) return fail(E3_DOMAIN, "top_k must be >= 1");
+  if (cfg->top_k > E3_MAX_TOP_K)
+    return fail(E3_DOMAIN, "top_k above " + std::to_string(E3_MAX_TOP_K) + " is not supported");
+  const uint64_t M = ds->M;
+  uint64_t total = 0;
+  if (int rc = e3_num_combinations(M, 3, &total)) return rc;
+  const uint64_t r0 = cfg->rank_begin;
+  const uint64_t r1 = cfg->rank_end == 0 ? total : cfg->rank_end;
+  if (r1 > total || r0 > r1) return fail(E3_INDEX, "triple-rank range outside [0, C(M,3))");
+  *n_top = 0;
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (r0 == r1) return E3_OK;
+  CUDA_TRY(cudaSetDevice(ds->device));
+
+  uint32_t t0[3], t1[3];
+  e3::triple_unrank(M, r0, t0);
+  e3::triple_unrank(M, r1 - 1, t1);
+  SearchArgs a;
+  a.item_begin = ds->h_itemoff[t0[0]];
+  a.item_count = ds->h_itemoff[t1[0] + 1] - a.item_begin;
+  a.rank_begin = r0;
+  a.rank_end = r1;
+  a.top_k = cfg->top_k;
+  a.gthr = ds->gthr;
+  const bool ranged = !(r0 == 0 && r1 == total);
+
+  const uint32_t K = cfg->top_k;
+  const uint64_t grid64 = std::min<uint64_t>(uint64_t(ds->num_sms) * ds->search_ctas_per_sm,
+                                             a.item_count);
+  const uint32_t grid = uint32_t(std::max<uint64_t>(1, grid64));
+  const uint32_t nlists = grid * kWarps;
+  const size_t need = size_t(nlists) * K;
+  if (need > ds->lists_cap) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(ds->lists[b]);
+      cudaFree(ds->counts[b]);
+      ds->lists[b] = nullptr;
+      ds->counts[b] = nullptr;
+      CUDA_TRY(cudaMalloc(&ds->lists[b], sizeof(ulonglong2) * need));
+      CUDA_TRY(cudaMalloc(&ds->counts[b], sizeof(uint32_t) * nlists));
+    }
+    ds->lists_cap = need;
+  }
+  a.out_lists = ds->lists[0];
+  a.out_counts = ds->counts[0];
+  const DevData d = dev_view(ds);
+  const size_t smem = 2 * sizeof(uint64_t) * kWarps * K;
+
+  cudaStream_t st = ds->stream;
+  CUDA_TRY(cudaEventRecord(ds->ev[0], st));
+  CUDA_TRY(cudaMemsetAsync(ds->gthr, 0xff, sizeof(uint64_t), st));
+  CUDA_TRY(cudaEventRecord(ds->ev[1], st));
+  if (ranged)
+    search_kernel<true><<<grid, kWarps * 32, smem, st>>>(d, a);
+  else
+    search_kernel<false><<<grid, kWarps * 32, smem, st>>>(d, a);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(ds->ev[2], st));
+  uint32_t launches = 1;
+  // Merge rounds: groups of lists -> one list each, until one list remains.
+  uint32_t nl = nlists;
+  int cur = 0;
+  const uint32_t group = std::max<uint32_t>(2, kMergeCap / K);
+  while (nl > 1) {
+    const uint32_t g = std::min(group, nl);
+    uint32_t P = 1;
+    while (P < g * K) P <<= 1;
+    const uint32_t blocks = (nl + g - 1) / g;
+    merge_kernel<<<blocks, 1024, sizeof(ulonglong2) * P, st>>>(
+        ds->lists[cur], ds->counts[cur], nl, K, g, P, ds->lists[cur ^ 1], ds->counts[cur ^ 1]);
+    CUDA_TRY(cudaGetLastError());
+    ++launches;
+    cur ^= 1;
+    nl = blocks;
+  }
+  std::vector<ulonglong2> h(K);
+  uint32_t cnt = 0;
+  CUDA_TRY(cudaMemcpyAsync(h.data(), ds->lists[cur], sizeof(ulonglong2) * K,
+                           cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&cnt, ds->counts[cur], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(ds->ev[3], st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  cnt = std::min(cnt, K);
+  for (uint32_t x = 0; x < cnt; ++x) {
+    top[x].score = key_score(h[x].x);
+    top[x].i0 = uint32_t(h[x].y >> 42);
+    top[x].i1 = uint32_t((h[x].y >> 21) & 0x1fffff);
+    top[x].i2 = uint32_t(h[x].y & 0x1fffff);
+    top[x]._pad = 0;
+  }
+  *n_top = cnt;
+  if (stats) {
+    float ms = 0.f;
+    stats->combinations = r1 - r0;
+    cudaEventElapsedTime(&ms, ds->ev[1], ds->ev[2]);
+    stats->kernel_ms = ms;
+    cudaEventElapsedTime(&ms, ds->ev[0], ds->ev[3]);
+    stats->total_device_ms = ms;
+    stats->kernel_launches = launches;
+    stats->elapsed_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  }
+  return E3_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI: tables and scores for explicit triples
+// ---------------------------------------------------------------------------
+namespace {
+int run_triples(const e3_dataset* ds, const uint32_t* triples, uint64_t n, uint32_t* tables,
+                double* scores) {
+  if (!ds) return fail(E3_DOMAIN, "null dataset");
+  for (uint64_t t = 0; t < n; ++t) {
+    const uint32_t i = triples[3 * t], j = triples[3 * t + 1], k = triples[3 * t + 2];
+    if (!(i < j && j < k))
+      return fail(E3_INDEX, "triple (" + std::to_string(i) + "," + std::to_string(j) + "," +
+                                std::to_string(k) + ") is not strictly ordered");
+    if (k >= ds->M)
+      return fail(E3_INDEX, "triple (" + std::to_string(i) + "," + std::to_string(j) + "," +
+                                std::to_string(k) + ") out of range for " +
+                                std::to_string(ds->M) + " SNPs");
+  }
+  if (n == 0) return E3_OK;
+  CUDA_TRY(cudaSetDevice(ds->device));
+  uint32_t* d_tri = nullptr;
+  uint32_t* d_tab = nullptr;
+  double* d_sc = nullptr;
+  CUDA_TRY(cudaMalloc(&d_tri, sizeof(uint32_t) * 3 * n));
+  if (tables) CUDA_TRY(cudaMalloc(&d_tab, sizeof(uint32_t) * 54 * n));
+  if (scores) CUDA_TRY(cudaMalloc(&d_sc, sizeof(double) * n));
+  cudaStream_t st = ds->stream;
+  CUDA_TRY(cudaMemcpyAsync(d_tri, triples, sizeof(uint32_t) * 3 * n, cudaMemcpyHostToDevice, st));
+  triples_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(dev_view(ds), d_tri, n, d_tab, d_sc);
+  CUDA_TRY(cudaGetLastError());
+  if (tables)
+    CUDA_TRY(cudaMemcpyAsync(tables, d_tab, sizeof(uint32_t) * 54 * n, cudaMemcpyDeviceToHost, st));
+  if (scores)
+    CUDA_TRY(cudaMemcpyAsync(scores, d_sc, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFree(d_tri);
+  cudaFree(d_tab);
+  cudaFree(d_sc);
+  return E3_OK;
+}
+}  // namespace
+
+extern "C" int e3_tables(const e3_dataset* ds, const uint32_t* triples, uint64_t n,
+                         uint32_t* out) {
+  return run_triples(ds, triples, n, out, nullptr);
+}
+
+extern "C" int e3_scores(const e3_dataset* ds, const uint32_t* triples, uint64_t n,
+                         double* out) {
+  return run_triples(ds, triples, n, nullptr, out);
+}

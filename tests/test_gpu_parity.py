@@ -1,0 +1,181 @@
+"""Parity of the CUDA path (called through the C ABI) with the reference:
+bit-exact tables, identical best/top-k triples and bit-identical K2 scores,
+against golden outputs of the reference itself and against the oracle on
+seeded inputs. Full-size configs are checked through size-independent
+properties: random triple-rank ranges vs the oracle, oracle re-scoring of the
+GPU top-k, the planted triple, and partition+merge == whole."""
+import numpy as np
+import pytest
+
+import py_oracle as po
+from helpers import assert_hits_identical, hits_of, product_dataset, ref_hits
+from paper_2201_10956_b200 import epi3
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    assert epi3.device_count() >= 1, "no CUDA device: the product has no CPU fallback"
+
+
+def _random_ds(M, n0, n1, seed):
+    rng = np.random.default_rng(seed)
+    geno = rng.integers(0, 3, (M, n0 + n1), dtype=np.uint8)
+    pheno = np.array([0] * n0 + [1] * n1, dtype=np.uint8)
+    rng.shuffle(pheno)
+    return epi3.binarize(geno, pheno)
+
+
+def test_tables_bit_exact_vs_reference(golden):
+    n = 0
+    for case in golden["cases"]:
+        if "tables" not in case:
+            continue
+        with epi3.DeviceDataset(product_dataset(case)) as dd:
+            got = dd.tables(case["triples"])
+        assert got.tolist() == case["tables"], case["name"]
+        n += len(case["triples"])
+    assert n > 500
+
+
+@pytest.mark.parametrize("M,n0,n1,seed", [(9, 1, 1, 1), (12, 31, 33, 2), (16, 200, 57, 3),
+                                          (10, 0, 77, 4), (10, 129, 0, 5), (40, 513, 511, 6)])
+def test_all_tables_and_scores_vs_oracle(M, n0, n1, seed):
+    ds = _random_ds(M, n0, n1, seed)
+    od = po.OracleDataset.of(ds)
+    P = od.log_table()
+    triples = [(a, b, c) for a in range(M) for b in range(a + 1, M) for c in range(b + 1, M)]
+    with epi3.DeviceDataset(ds) as dd:
+        tabs = dd.tables(triples)
+        scores = dd.scores(triples)
+    for t, tab, s in zip(triples, tabs, scores):
+        expect = od.table(t)
+        assert (tab == expect).all(), t
+        assert float(s).hex() == po.k2_score(expect, P).hex(), t
+
+
+def test_search_matches_reference_golden(golden):
+    for case in golden["cases"]:
+        expect = ref_hits(case["search"])
+        with epi3.DeviceDataset(product_dataset(case)) as dd:
+            res = dd.search(epi3.SearchConfig(top_k=len(expect)))
+        assert_hits_identical(hits_of(res), expect)
+        assert res.best.triple == tuple(case["search"]["best"]["triple"]), case["name"]
+        assert res.stats.combinations_evaluated == case["search"]["combinations"]
+
+
+def test_tie_breaks_to_lexicographically_smallest(golden_cases):
+    case = golden_cases["tie_dup_snp"]
+    res = epi3.run_search(product_dataset(case), epi3.SearchConfig(top_k=10))
+    assert res.best.triple == (2, 5, 7)
+    s = {h.triple: h.score for h in res.top}
+    assert s[(2, 5, 7)] == s[(2, 7, 9)]
+
+
+def test_planted_recovery(golden):
+    # acceptance.cpp:212-229: >= 19/20 recovered, and identical to the reference
+    plant = [c for c in golden["cases"] if c["name"].startswith("plant_seed")]
+    assert len(plant) == 20
+    hit = sum(epi3.run_search(product_dataset(c), epi3.SearchConfig(top_k=1)).best.triple
+              == (4, 13, 27) for c in plant)
+    assert hit >= 19
+
+
+@pytest.mark.parametrize("top_k", [1, 2, 17, 100, 256])
+def test_top_k_sizes_vs_oracle(top_k):
+    ds = _random_ds(40, 300, 211, 11)
+    od = po.OracleDataset.of(ds)
+    res = epi3.run_search(ds, epi3.SearchConfig(top_k=top_k))
+    assert_hits_identical(hits_of(res), od.search(top_k=top_k))
+    assert res.top[0] == res.best
+
+
+def test_ranged_searches_vs_oracle():
+    ds = _random_ds(90, 700, 300, 12)
+    od = po.OracleDataset.of(ds)
+    total = epi3.num_combinations(90, 3)
+    rng = np.random.default_rng(13)
+    with epi3.DeviceDataset(ds) as dd:
+        for _ in range(12):
+            a, b = sorted(int(x) for x in rng.integers(0, total + 1, 2))
+            res = dd.search(epi3.SearchConfig(top_k=7, rank_begin=a, rank_end=b))
+            assert res.stats.combinations_evaluated == b - a
+            assert_hits_identical(hits_of(res), od.search(top_k=7, r0=a, r1=b))
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_partition_then_merge_equals_whole(G):
+    # the multi-GPU contract: equal-work ranges searched independently and
+    # merged with reduce_results == one full search (search_test.cpp:212-242)
+    ds = _random_ds(120, 600, 600, 14)
+    with epi3.DeviceDataset(ds) as dd:
+        whole = dd.search(epi3.SearchConfig(top_k=25))
+        parts = [dd.search(epi3.SearchConfig(top_k=25, rank_begin=a, rank_end=b))
+                 for a, b in epi3.partition(120, G)]
+    merged = epi3.reduce_results(parts)
+    assert merged.best == whole.best and merged.top == whole.top
+    assert merged.stats.combinations_evaluated == epi3.num_combinations(120, 3)
+
+
+def test_deterministic_repeats():
+    ds = _random_ds(64, 400, 400, 15)
+    with epi3.DeviceDataset(ds) as dd:
+        a = dd.search(epi3.SearchConfig(top_k=50))
+        for _ in range(3):
+            assert epi3.same_outcome(a, dd.search(epi3.SearchConfig(top_k=50)))
+
+
+def test_errors_are_loud():
+    ds = _random_ds(10, 20, 20, 16)
+    with epi3.DeviceDataset(ds) as dd:
+        with pytest.raises(epi3.IndexError):
+            dd.tables([(3, 2, 5)])
+        with pytest.raises(epi3.IndexError):
+            dd.tables([(0, 1, 10)])
+        with pytest.raises(epi3.DomainError):
+            dd.search(epi3.SearchConfig(top_k=0))
+        with pytest.raises(epi3.DomainError):
+            dd.search(epi3.SearchConfig(top_k=epi3.MAX_TOP_K + 1))
+        with pytest.raises(epi3.IndexError):
+            dd.search(epi3.SearchConfig(rank_begin=5, rank_end=1000))
+    bad = _random_ds(5, 70, 0, 17)
+    bad.ctrl[0, 1] |= bad.ctrl[0, 0]  # overlapping planes
+    with pytest.raises(epi3.DomainError):
+        epi3.DeviceDataset(bad)
+    bad = _random_ds(5, 70, 0, 18)
+    bad.ctrl[2, 0, -1] |= np.uint64(1) << np.uint64(63)  # dirty padding
+    with pytest.raises(epi3.DomainError):
+        epi3.DeviceDataset(bad)
+
+
+def _config_dataset(M, N, n1, seed):
+    plant = epi3.PlantSpec((M // 8, M // 2, 7 * M // 8), (1, 1, 1), 0.9,
+                           0.468 if 2 * n1 == N else 0.198)
+    geno, pheno = epi3.generate_synthetic(M, N, 0.3, seed, plant, exact_cases=n1)
+    return epi3.binarize(geno, pheno), plant.triple
+
+
+@pytest.mark.parametrize("name,M,N,n1,top_k,ranges", [
+    ("cfg3", 8192, 16384, 8192, 10, 3),
+    ("cfg4", 1024, 262144, 131072, 10, 2),
+    ("cfg5", 4096, 32768, 8192, 100, 3),
+])
+def test_full_size_configs_by_ranges(name, M, N, n1, top_k, ranges):
+    """BASELINE configs 3-5 at full size: random triple-rank windows vs the
+    oracle (identical top-k, bit-identical scores) plus oracle re-scoring."""
+    ds, planted = _config_dataset(M, N, n1, {"cfg3": 1003, "cfg4": 1004, "cfg5": 1005}[name])
+    od = po.OracleDataset.of(ds)
+    P = od.log_table()
+    total = epi3.num_combinations(M, 3)
+    rng = np.random.default_rng(M)
+    window = 200_000 if N <= 32768 else 20_000
+    with epi3.DeviceDataset(ds) as dd:
+        r_pl = epi3.triple_rank(M, planted)
+        starts = [max(0, r_pl - window // 2)] + [int(x) for x in rng.integers(0, total - window, ranges)]
+        for a in starts:
+            res = dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=a + window))
+            assert_hits_identical(hits_of(res), od.search(top_k=top_k, r0=a, r1=a + window))
+        got = dd.scores([h.triple for h in res.top])
+        for h, s in zip(res.top, got):
+            assert s.hex() == h.score.hex() == po.k2_score(od.table(h.triple), P).hex()
