@@ -253,7 +253,11 @@ def main():
         traffic = None
         prof = ROOT / "profiles" / "roofline_traffic.json"
         if prof.exists():
-            traffic = json.loads(prof.read_text()).get(args.workload)
+            t = json.loads(prof.read_text()).get(args.workload)
+            if t:  # ncu dram read+write of one launch, scaled to this step's triples
+                traffic = {"dram_bytes_per_launch": t["dram_bytes_per_triple"] * elements / N
+                           / args.steps, "from": f"profiles/{t['round']}_search_{args.workload}"
+                                                 "_raw.csv (per-triple, scaled)"}
         cpu = None
         if world == 1 and not args.no_cpu:
             with tempfile.TemporaryDirectory() as d:

@@ -1,0 +1,4 @@
+// Forwarding header: the reference include path epi3/kernels.hpp maps to the
+// single drop-in surface of the B200 engine.
+#pragma once
+#include "epi3/api.hpp"

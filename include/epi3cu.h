@@ -7,7 +7,7 @@
  * every entry point returns an e3_status and e3_last_error() holds the
  * thread-local message, mirroring the epi3::Error hierarchy
  * (include/epi3/common.hpp:36-105). The C++ mirror of the reference API
- * (include/epi3/*.hpp in this repo) is implemented on top of these calls.
+ * (include/epi3/api.hpp in this repo) is implemented on top of these calls.
  *
  * Threading: calls on distinct datasets are independent; one e3_search per
  * dataset at a time (a dataset owns one CUDA stream).
