@@ -151,6 +151,8 @@ def main():
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--slices", type=int, default=64,
                     help="a step searches 1/SLICES of the triple-rank space per GPU")
+    ap.add_argument("--engine", default="tc", choices=["tc", "popc"],
+                    help="tc: tcgen05 kind::i8 GEMM kernel (default); popc: LOP3/POPC kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -187,7 +189,7 @@ def main():
     dd = epi3.DeviceDataset(ds, device=local)
     for s in range(args.warmup):
         a, b = slice_of(s)
-        dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b))
+        dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b, engine=args.engine))
     barrier()
     sampler = ClockSampler(local)
     sampler.start()
@@ -197,7 +199,7 @@ def main():
         l2_flush.zero_()
         torch.cuda.synchronize()
         a, b = slice_of(args.warmup + s)
-        r = dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b))
+        r = dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b, engine=args.engine))
         dev_ms += r.stats.total_device_ms
         kern_ms += r.stats.kernel_ms
         launches += r.stats.kernel_launches
@@ -218,7 +220,7 @@ def main():
             a, b = slice_of(s)
             with epi3.DeviceDataset(ds, local, ctypes.c_void_p(pin_ctrl.data_ptr()),
                                     ctypes.c_void_p(pin_cases.data_ptr())) as d2:
-                d2.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b))
+                d2.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b, engine=args.engine))
         barrier()
         t0 = time.perf_counter()
         e2e_el = 0
@@ -226,7 +228,7 @@ def main():
             a, b = slice_of(args.warmup + s)
             with epi3.DeviceDataset(ds, local, ctypes.c_void_p(pin_ctrl.data_ptr()),
                                     ctypes.c_void_p(pin_cases.data_ptr())) as d2:
-                d2.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b))
+                d2.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b, engine=args.engine))
             e2e_el += (b - a) * N
         barrier()
         e2e_s = time.perf_counter() - t0

@@ -56,12 +56,15 @@ typedef struct {
  * or rank_end == 0 — is the full search run_search performs (search.cpp:127). */
 typedef struct {
   uint32_t top_k;       /* >= 1, <= E3_MAX_TOP_K */
-  uint32_t flags;       /* reserved, 0 */
+  uint32_t flags;       /* 0 = default engine (tensor cores); E3_ENGINE_POPC = LOP3/POPC kernel */
   uint64_t rank_begin;
   uint64_t rank_end;    /* 0 = C(M,3) */
 } e3_search_cfg;
 
 #define E3_MAX_TOP_K 256u
+/* Engine selection (e3_search_cfg.flags). Both engines produce identical
+ * results; the default is the tcgen05 kind::i8 GEMM formulation. */
+#define E3_ENGINE_POPC 1u
 
 /* Replaces SearchStats (search.hpp:37-41). */
 typedef struct {

@@ -39,6 +39,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -178,7 +179,35 @@ __device__ __forceinline__ void count_quad(const uint4& i0, const uint4& i1, con
   count_word(i0.w, i1.w, j0.w, j1.w, k0.w, k1.w, T);
 }
 
-// Accumulates one class of the CTA item into T[q][8] for this lane.
+// Carry-save adder: a + b + c == s + 2*cy, bitwise. Two LOP3s (0x96, 0xE8).
+__device__ __forceinline__ void csa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s,
+                                    uint32_t& cy) {
+  s = a ^ b ^ c;
+  cy = (a & b) | (c & (a ^ b));
+}
+
+// popc(v0)+...+popc(v7) with 4 POPC instead of 8: a 8:4 carry-save tree
+// (ones, twos, 2x fours) moves work from the quarter-rate POPC (XU) pipe to
+// the full-rate LOP3 (ALU) pipe; the weights are applied with IMAD (FMA pipe).
+__device__ __forceinline__ uint32_t count8_csa(const uint32_t (&v)[8]) {
+  uint32_t s1, c1, s2, c2, s3, c3, t1, f1;
+  csa(v[0], v[1], v[2], s1, c1);
+  csa(v[3], v[4], v[5], s2, c2);
+  csa(s1, s2, v[6], s3, c3);
+  const uint32_t ones = s3 ^ v[7], c4 = s3 & v[7];
+  csa(c1, c2, c3, t1, f1);
+  const uint32_t twos = t1 ^ c4, f2 = t1 & c4;
+  return __popc(ones) + 2u * __popc(twos) + 4u * (__popc(f1) + __popc(f2));
+}
+
+// Cells counted with plain POPC; the rest go through count8_csa. Two plain
+// cells balance the XU (16/clk/SM) and ALU (64/clk/SM) pipes:
+// per 8 triple-words ALU 2*12 + 6*22 = 156 ops, XU 2*8 + 6*4 = 40 ops.
+constexpr int kPlainCells = 2;
+
+// Accumulates one class of the CTA item into T[q][8] for this lane, two
+// word-quads (256 samples) per step; the plane buffers carry one zero quad of
+// padding so an odd quad count needs no tail code.
 __device__ __forceinline__ void accumulate_class(const uint4* __restrict__ planes, uint32_t wq,
                                                  uint32_t M, uint32_t i, const uint32_t* jc,
                                                  uint32_t kc, uint32_t (&T)[kJPerWarp][8]) {
@@ -189,13 +218,41 @@ __device__ __forceinline__ void accumulate_class(const uint4* __restrict__ plane
   const size_t row = size_t(M) * 2;
   const uint4* p = planes;
 #pragma unroll 1
-  for (uint32_t w = 0; w < wq; ++w, p += row) {
-    const uint4 i0 = __ldg(p + 2 * i), i1 = __ldg(p + 2 * i + 1);
-    const uint4 k0 = __ldg(p + 2 * kc), k1 = __ldg(p + 2 * kc + 1);
+  for (uint32_t w = 0; w < wq; w += 2, p += 2 * row) {
+    uint32_t I[2][8], K[2][8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint4 a = __ldg(p + h * row + 2 * i + g), b = __ldg(p + h * row + 2 * kc + g);
+        I[g][4 * h] = a.x; I[g][4 * h + 1] = a.y; I[g][4 * h + 2] = a.z; I[g][4 * h + 3] = a.w;
+        K[g][4 * h] = b.x; K[g][4 * h + 1] = b.y; K[g][4 * h + 2] = b.z; K[g][4 * h + 3] = b.w;
+      }
 #pragma unroll
     for (int q = 0; q < kJPerWarp; ++q) {
-      const uint4 j0 = __ldg(p + 2 * jc[q]), j1 = __ldg(p + 2 * jc[q] + 1);
-      count_quad(i0, i1, j0, j1, k0, k1, T[q]);
+      uint32_t J[2][8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const uint4 b = __ldg(p + h * row + 2 * jc[q] + g);
+          J[g][4 * h] = b.x; J[g][4 * h + 1] = b.y; J[g][4 * h + 2] = b.z; J[g][4 * h + 3] = b.w;
+        }
+#pragma unroll
+      for (int cell = 0; cell < 8; ++cell) {
+        const int a = cell >> 2, b = (cell >> 1) & 1, g = cell & 1;
+        uint32_t v[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) v[x] = I[a][x] & J[b][x] & K[g][x];
+        if (cell < kPlainCells) {
+          uint32_t s = 0;
+#pragma unroll
+          for (int x = 0; x < 8; ++x) s += __popc(v[x]);
+          T[q][cell] += s;
+        } else {
+          T[q][cell] += count8_csa(v);
+        }
+      }
     }
   }
 }
@@ -242,8 +299,8 @@ __device__ void warp_insert(uint64_t* ls, uint64_t* lt, uint32_t& n, uint32_t K,
   }
 }
 
-template <bool kRanged>
-__global__ void __launch_bounds__(kWarps * 32, 2)
+template <bool kRanged, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 search_kernel(const DevData d, const SearchArgs a) {
   extern __shared__ uint64_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -342,6 +399,12 @@ search_kernel(const DevData d, const SearchArgs a) {
   for (uint32_t e = lane; e < n; e += 32) a.out_lists[list * K + e] = make_ulonglong2(ls[e], lt[e]);
   if (lane == 0) a.out_counts[list] = n;
 }
+
+}  // namespace
+
+#include "search_tc.cuh"
+
+namespace {
 
 // Bitonic merge of `group` consecutive lists (each <= K sorted entries) into
 // one list of the K smallest entries under hit_less order.
@@ -489,11 +552,14 @@ struct e3_dataset {
   double* logp = nullptr;
   uint64_t* itemoff = nullptr;
   std::vector<uint64_t> h_itemoff;
-  int num_sms = 0, search_ctas_per_sm = 0;
+  uint64_t* itemoff_tc = nullptr;     // tensor-core kernel item prefix (32-j x 64-k tiles)
+  std::vector<uint64_t> h_itemoff_tc;
+  int num_sms = 0, search_ctas_per_sm = 0, search_min_blocks = 1;
   // scratch reused across searches
   ulonglong2* lists[2] = {nullptr, nullptr};
   uint32_t* counts[2] = {nullptr, nullptr};
   size_t lists_cap = 0;
+  uint32_t counts_cap = 0;
   uint64_t* gthr = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
@@ -512,6 +578,7 @@ void release(e3_dataset* ds) {
   }
   cudaFree(ds->logp);
   cudaFree(ds->itemoff);
+  cudaFree(ds->itemoff_tc);
   cudaFree(ds->gthr);
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
@@ -551,7 +618,10 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     ds->wq[c] = uint32_t((n + 127) / 128);
     CUDA_TRY(cudaMalloc(&ds->single[c], sizeof(uint2) * M));
     CUDA_TRY(cudaMalloc(&ds->pair[c], sizeof(uint4) * size_t(M) * M));
-    CUDA_TRY(cudaMalloc(&ds->planes[c], sizeof(uint4) * std::max<size_t>(1, size_t(ds->wq[c]) * M * 2)));
+    // one extra zero quad: the search kernel steps two quads at a time
+    const size_t plane_bytes = sizeof(uint4) * (size_t(ds->wq[c]) + 1) * M * 2;
+    CUDA_TRY(cudaMalloc(&ds->planes[c], plane_bytes));
+    CUDA_TRY(cudaMemsetAsync(ds->planes[c], 0, plane_bytes, ds->stream));
     if (ds->wq[c] == 0) {
       CUDA_TRY(cudaMemsetAsync(ds->single[c], 0, sizeof(uint2) * M, ds->stream));
       CUDA_TRY(cudaMemsetAsync(ds->pair[c], 0, sizeof(uint4) * size_t(M) * M, ds->stream));
@@ -591,6 +661,19 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaMemcpyAsync(ds->itemoff, ds->h_itemoff.data(),
                            sizeof(uint64_t) * ds->h_itemoff.size(), cudaMemcpyHostToDevice,
                            ds->stream));
+  ds->h_itemoff_tc.assign(M - 1, 0);
+  for (uint32_t i = 0; i + 2 < M; ++i)
+    ds->h_itemoff_tc[i + 1] = ds->h_itemoff_tc[i] + tc::items_of(M, i);
+  CUDA_TRY(cudaMalloc(&ds->itemoff_tc, sizeof(uint64_t) * ds->h_itemoff_tc.size()));
+  CUDA_TRY(cudaMemcpyAsync(ds->itemoff_tc, ds->h_itemoff_tc.data(),
+                           sizeof(uint64_t) * ds->h_itemoff_tc.size(), cudaMemcpyHostToDevice,
+                           ds->stream));
+  CUDA_TRY(cudaFuncSetAttribute(tc::search_tc_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(tc::smem_bytes(E3_MAX_TOP_K))));
+  CUDA_TRY(cudaFuncSetAttribute(tc::search_tc_kernel<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(tc::smem_bytes(E3_MAX_TOP_K))));
   CUDA_TRY(cudaMalloc(&ds->gthr, sizeof(uint64_t)));
   uint32_t h_bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
@@ -602,15 +685,26 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
                 "set padding bits)");
   CUDA_TRY(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(ulonglong2) * 2 * kMergeCap)));
-  CUDA_TRY(cudaFuncSetAttribute(search_kernel<false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K)));
-  CUDA_TRY(cudaFuncSetAttribute(search_kernel<true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K)));
+  const int list_smem = int(2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K);
+  CUDA_TRY(cudaFuncSetAttribute(search_kernel<false, 1>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem));
+  CUDA_TRY(cudaFuncSetAttribute(search_kernel<true, 1>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem));
+  CUDA_TRY(cudaFuncSetAttribute(search_kernel<false, 2>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem));
+  CUDA_TRY(cudaFuncSetAttribute(search_kernel<true, 2>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem));
+  // E3_SEARCH_OCCUPANCY=1|2 selects the register/occupancy trade-off of the
+  // search kernel (tuning knob; the default is the measured best).
+  const char* occ_env = std::getenv("E3_SEARCH_OCCUPANCY");
+  ds->search_min_blocks = (occ_env && std::atoi(occ_env) == 1) ? 1 : 2;
   int occ = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ, search_kernel<false>, kWarps * 32, 2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K));
+  if (ds->search_min_blocks == 2)
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_kernel<false, 2>,
+                                                           kWarps * 32, list_smem));
+  else
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_kernel<false, 1>,
+                                                           kWarps * 32, list_smem));
   ds->search_ctas_per_sm = std::max(1, occ);
   return E3_OK;
 }
@@ -692,12 +786,23 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   const bool ranged = !(r0 == 0 && r1 == total);
 
   const uint32_t K = cfg->top_k;
-  const uint64_t grid64 = std::min<uint64_t>(uint64_t(ds->num_sms) * ds->search_ctas_per_sm,
-                                             a.item_count);
-  const uint32_t grid = uint32_t(std::max<uint64_t>(1, grid64));
-  const uint32_t nlists = grid * kWarps;
+  // Engine: tensor-core GEMM formulation by default; the POPC kernel on request.
+  const bool use_tc = !(cfg->flags & E3_ENGINE_POPC);
+  uint32_t grid, nlists;
+  tc::TcArgs ta{};
+  if (use_tc) {
+    ta.item_begin = ds->h_itemoff_tc[t0[0]];
+    ta.item_count = ds->h_itemoff_tc[t1[0] + 1] - ta.item_begin;
+    grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(ds->num_sms, ta.item_count)));
+    nlists = grid * tc::kEpilogueWarps;
+  } else {
+    const uint64_t grid64 = std::min<uint64_t>(uint64_t(ds->num_sms) * ds->search_ctas_per_sm,
+                                               a.item_count);
+    grid = uint32_t(std::max<uint64_t>(1, grid64));
+    nlists = grid * kWarps;
+  }
   const size_t need = size_t(nlists) * K;
-  if (need > ds->lists_cap) {
+  if (need > ds->lists_cap || nlists > ds->counts_cap) {
     for (int b = 0; b < 2; ++b) {
       cudaFree(ds->lists[b]);
       cudaFree(ds->counts[b]);
@@ -707,6 +812,7 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
       CUDA_TRY(cudaMalloc(&ds->counts[b], sizeof(uint32_t) * nlists));
     }
     ds->lists_cap = need;
+    ds->counts_cap = nlists;
   }
   a.out_lists = ds->lists[0];
   a.out_counts = ds->counts[0];
@@ -717,10 +823,24 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   CUDA_TRY(cudaEventRecord(ds->ev[0], st));
   CUDA_TRY(cudaMemsetAsync(ds->gthr, 0xff, sizeof(uint64_t), st));
   CUDA_TRY(cudaEventRecord(ds->ev[1], st));
-  if (ranged)
-    search_kernel<true><<<grid, kWarps * 32, smem, st>>>(d, a);
-  else
-    search_kernel<false><<<grid, kWarps * 32, smem, st>>>(d, a);
+  if (use_tc) {
+    ta.rank_begin = r0;
+    ta.rank_end = r1;
+    ta.top_k = K;
+    ta.gthr = ds->gthr;
+    ta.out_lists = ds->lists[0];
+    ta.out_counts = ds->counts[0];
+    ta.itemoff = ds->itemoff_tc;
+    const size_t tsm = tc::smem_bytes(K);
+    if (ranged) tc::search_tc_kernel<true><<<grid, tc::kThreads, tsm, st>>>(d, ta);
+    else tc::search_tc_kernel<false><<<grid, tc::kThreads, tsm, st>>>(d, ta);
+  } else if (ds->search_min_blocks == 2) {
+    if (ranged) search_kernel<true, 2><<<grid, kWarps * 32, smem, st>>>(d, a);
+    else search_kernel<false, 2><<<grid, kWarps * 32, smem, st>>>(d, a);
+  } else {
+    if (ranged) search_kernel<true, 1><<<grid, kWarps * 32, smem, st>>>(d, a);
+    else search_kernel<false, 1><<<grid, kWarps * 32, smem, st>>>(d, a);
+  }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(ds->ev[2], st));
   uint32_t launches = 1;

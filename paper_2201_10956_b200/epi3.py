@@ -95,6 +95,7 @@ class e3_plant(C.Structure):
 
 
 MAX_TOP_K = 256
+ENGINES = {"tc": 0, "popc": 1}  # e3_search_cfg.flags (E3_ENGINE_POPC = 1)
 _P = C.c_void_p
 _U64 = C.c_uint64
 _U32 = C.c_uint32
@@ -328,6 +329,7 @@ class SearchConfig:
     top_k: int = 10
     rank_begin: int = 0
     rank_end: int = 0  # 0 = C(M,3)
+    engine: str = "tc"  # "tc": tcgen05 kind::i8 GEMM kernel; "popc": LOP3/POPC kernel
 
 
 def same_outcome(a: SearchResult, b: SearchResult) -> bool:
@@ -418,7 +420,9 @@ class DeviceDataset:
         self.close()
 
     def search(self, cfg: SearchConfig = SearchConfig()) -> SearchResult:
-        c = e3_search_cfg(cfg.top_k, 0, cfg.rank_begin, cfg.rank_end)
+        if cfg.engine not in ENGINES:
+            raise DomainError(f"unknown engine {cfg.engine!r}")
+        c = e3_search_cfg(cfg.top_k, ENGINES[cfg.engine], cfg.rank_begin, cfg.rank_end)
         top = (e3_hit * max(1, cfg.top_k))()
         n = _U32()
         st = e3_stats()

@@ -55,11 +55,12 @@ def test_all_tables_and_scores_vs_oracle(M, n0, n1, seed):
         assert float(s).hex() == po.k2_score(expect, P).hex(), t
 
 
-def test_search_matches_reference_golden(golden):
+@pytest.mark.parametrize("engine", ["tc", "popc"])
+def test_search_matches_reference_golden(golden, engine):
     for case in golden["cases"]:
         expect = ref_hits(case["search"])
         with epi3.DeviceDataset(product_dataset(case)) as dd:
-            res = dd.search(epi3.SearchConfig(top_k=len(expect)))
+            res = dd.search(epi3.SearchConfig(top_k=len(expect), engine=engine))
         assert_hits_identical(hits_of(res), expect)
         assert res.best.triple == tuple(case["search"]["best"]["triple"]), case["name"]
         assert res.stats.combinations_evaluated == case["search"]["combinations"]
@@ -82,16 +83,18 @@ def test_planted_recovery(golden):
     assert hit >= 19
 
 
+@pytest.mark.parametrize("engine", ["tc", "popc"])
 @pytest.mark.parametrize("top_k", [1, 2, 17, 100, 256])
-def test_top_k_sizes_vs_oracle(top_k):
+def test_top_k_sizes_vs_oracle(top_k, engine):
     ds = _random_ds(40, 300, 211, 11)
     od = po.OracleDataset.of(ds)
-    res = epi3.run_search(ds, epi3.SearchConfig(top_k=top_k))
+    res = epi3.run_search(ds, epi3.SearchConfig(top_k=top_k, engine=engine))
     assert_hits_identical(hits_of(res), od.search(top_k=top_k))
     assert res.top[0] == res.best
 
 
-def test_ranged_searches_vs_oracle():
+@pytest.mark.parametrize("engine", ["tc", "popc"])
+def test_ranged_searches_vs_oracle(engine):
     ds = _random_ds(90, 700, 300, 12)
     od = po.OracleDataset.of(ds)
     total = epi3.num_combinations(90, 3)
@@ -99,19 +102,20 @@ def test_ranged_searches_vs_oracle():
     with epi3.DeviceDataset(ds) as dd:
         for _ in range(12):
             a, b = sorted(int(x) for x in rng.integers(0, total + 1, 2))
-            res = dd.search(epi3.SearchConfig(top_k=7, rank_begin=a, rank_end=b))
+            res = dd.search(epi3.SearchConfig(top_k=7, rank_begin=a, rank_end=b, engine=engine))
             assert res.stats.combinations_evaluated == b - a
             assert_hits_identical(hits_of(res), od.search(top_k=7, r0=a, r1=b))
 
 
+@pytest.mark.parametrize("engine", ["tc", "popc"])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-def test_partition_then_merge_equals_whole(G):
+def test_partition_then_merge_equals_whole(G, engine):
     # the multi-GPU contract: equal-work ranges searched independently and
     # merged with reduce_results == one full search (search_test.cpp:212-242)
     ds = _random_ds(120, 600, 600, 14)
     with epi3.DeviceDataset(ds) as dd:
-        whole = dd.search(epi3.SearchConfig(top_k=25))
-        parts = [dd.search(epi3.SearchConfig(top_k=25, rank_begin=a, rank_end=b))
+        whole = dd.search(epi3.SearchConfig(top_k=25, engine=engine))
+        parts = [dd.search(epi3.SearchConfig(top_k=25, rank_begin=a, rank_end=b, engine=engine))
                  for a, b in epi3.partition(120, G)]
     merged = epi3.reduce_results(parts)
     assert merged.best == whole.best and merged.top == whole.top
@@ -156,12 +160,13 @@ def _config_dataset(M, N, n1, seed):
     return epi3.binarize(geno, pheno), plant.triple
 
 
+@pytest.mark.parametrize("engine", ["tc", "popc"])
 @pytest.mark.parametrize("name,M,N,n1,top_k,ranges", [
     ("cfg3", 8192, 16384, 8192, 10, 3),
     ("cfg4", 1024, 262144, 131072, 10, 2),
     ("cfg5", 4096, 32768, 8192, 100, 3),
 ])
-def test_full_size_configs_by_ranges(name, M, N, n1, top_k, ranges):
+def test_full_size_configs_by_ranges(name, M, N, n1, top_k, ranges, engine):
     """BASELINE configs 3-5 at full size: random triple-rank windows vs the
     oracle (identical top-k, bit-identical scores) plus oracle re-scoring."""
     ds, planted = _config_dataset(M, N, n1, {"cfg3": 1003, "cfg4": 1004, "cfg5": 1005}[name])
@@ -174,8 +179,21 @@ def test_full_size_configs_by_ranges(name, M, N, n1, top_k, ranges):
         r_pl = epi3.triple_rank(M, planted)
         starts = [max(0, r_pl - window // 2)] + [int(x) for x in rng.integers(0, total - window, ranges)]
         for a in starts:
-            res = dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=a + window))
+            res = dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=a + window,
+                                              engine=engine))
             assert_hits_identical(hits_of(res), od.search(top_k=top_k, r0=a, r1=a + window))
         got = dd.scores([h.triple for h in res.top])
         for h, s in zip(res.top, got):
             assert s.hex() == h.score.hex() == po.k2_score(od.table(h.triple), P).hex()
+
+
+def test_engines_agree_on_random_inputs():
+    rng = np.random.default_rng(99)
+    for rep in range(6):
+        M = int(rng.integers(3, 150))
+        n0, n1 = int(rng.integers(0, 700)), int(rng.integers(1, 700))
+        ds = _random_ds(M, n0, n1, 100 + rep)
+        with epi3.DeviceDataset(ds) as dd:
+            a = dd.search(epi3.SearchConfig(top_k=33, engine="tc"))
+            b = dd.search(epi3.SearchConfig(top_k=33, engine="popc"))
+        assert epi3.same_outcome(a, b), (M, n0, n1)
