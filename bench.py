@@ -51,6 +51,7 @@ WORKLOADS = {
 CPU_SAMPLE_SNPS = 512
 POPC_PER_SM_CLK = 16.0  # measured: tools/ipipe_bench.cu, profiles/r01_ipipe.txt
 ALG_POPC_PER_ELEMENT = 27.0 / 32.0  # 27 POPC per triple per 32-sample word
+TC_OPS_PER_ELEMENT = 16.0  # tensor engine: 8 int8 MACs per triplet x sample
 
 
 def env_int(name, default):
@@ -250,16 +251,34 @@ def main():
         kernel_rate = elements / (kern_ms / 1e3)  # one GPU's elements per second in the kernel
         f_mhz = clocks["sm_mhz"] or 1965.0
         nsm = torch.cuda.get_device_properties(local).multi_processor_count
-        peak = nsm * POPC_PER_SM_CLK * f_mhz * 1e6 / 1e12
-        achieved = kernel_rate * ALG_POPC_PER_ELEMENT / 1e12
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+            if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        if args.engine == "tc":
+            # GEMM formulation: 8 int8 MACs (16 ops) per triplet x sample
+            achieved = kernel_rate * TC_OPS_PER_ELEMENT / 1e12
+            bf16 = peaks.get("bf16_tflops", 1590.0)
+            peak = 2.0 * bf16  # dense int8 = 2x dense bf16 on B200
+            roof = {"bound": "tensor", "unit": "TOPS (int8, algorithmic)",
+                    "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (burst)" if peaks
+                                    else "2 x fallback 1590 TFLOP/s"),
+                    "note": "tcgen05.mma kind::i8: 8 MACs per element (4 (a,b) pair rows x 2 g "
+                            "columns); the 19 other cells per class come exactly from the "
+                            "marginal index"}
+        else:
+            peak = nsm * POPC_PER_SM_CLK * f_mhz * 1e6 / 1e12
+            achieved = kernel_rate * ALG_POPC_PER_ELEMENT / 1e12
+            roof = {"bound": "int-pipe POPC (SURVEY.md §8(d))", "unit": "T POPC/s (algorithmic, 27/word)",
+                    "effective": True,
+                    "issued_frac": kernel_rate * (5.0 / 32.0) / 1e12 / peak,
+                    "note": "27-POPC algorithmic basis (may exceed 1); the kernel issues 5 POPC "
+                            "per triple-word (marginal subtraction + carry-save)"}
         traffic = None
         prof = ROOT / "profiles" / "roofline_traffic.json"
         if prof.exists():
-            t = json.loads(prof.read_text()).get(args.workload)
+            t = json.loads(prof.read_text()).get(args.workload, {}).get(args.engine)
             if t:  # ncu dram read+write of one launch, scaled to this step's triples
                 traffic = {"dram_bytes_per_launch": t["dram_bytes_per_triple"] * elements / N
-                           / args.steps, "from": f"profiles/{t['round']}_search_{args.workload}"
-                                                 "_raw.csv (per-triple, scaled)"}
+                           / args.steps, "from": t["report"] + " (per-triple, scaled)"}
         cpu = None
         if world == 1 and not args.no_cpu:
             with tempfile.TemporaryDirectory() as d:
@@ -269,7 +288,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32 (bit-plane LOP3/POPC) + f64 (K2)",
+            "vs_baseline": None, "dtype": ("u8 (0/1 int8 MMA, s32 accumulate) + f64 (K2)" if args.engine == "tc"
+                      else "u32 (bit-plane LOP3/POPC) + f64 (K2)"),
             "data": "synthetic",
             "config": {"workload": desc, "top_k": top_k,
                        "step": f"one search over a 1/{args.slices} triple-rank slice "
@@ -285,18 +305,9 @@ def main():
                 "value": e2e["elements"] * world / e2e_secs / 1e12, "unit": UNIT,
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                 "ms_per_step": e2e_secs * 1e3 / args.steps},
-            "roofline": {
-                "bound": "int-pipe POPC (not hbm/tensor: SURVEY.md §8(d))",
-                "achieved": achieved, "peak": peak, "unit": "T POPC/s (algorithmic, 27/word)",
-                "frac": achieved / peak,
-                "effective": True,
-                "issued_frac": kernel_rate * (8.0 / 32.0) / 1e12 / peak,
-                "note": "kernel issues 8 POPC per triple-word (marginal subtraction) vs the "
-                        "27 of the reference formulation; frac uses 27 (may exceed 1), "
-                        "issued_frac the 8 actually issued; peak = 16 POPC/clk/SM (measured) "
-                        "x SMs x median SM clock under load",
-                "kernel_ms_per_step": kern_ms / args.steps,
-                "traffic": traffic},
+            "roofline": dict(roof, achieved=achieved, peak=peak, frac=achieved / peak,
+                             engine=args.engine, kernel_ms_per_step=kern_ms / args.steps,
+                             traffic=traffic),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -43,7 +43,7 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build_cuda(force: bool = False) -> Path:
     srcs = [CSRC / "engine.cu", CSRC / "host.cpp"]
-    deps = srcs + [CSRC / "internal.h", INCLUDE / "epi3cu.h"]
+    deps = srcs + sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh")) + [INCLUDE / "epi3cu.h"]
     if force or _stale(LIB_CU, deps):
         BUILD.mkdir(exist_ok=True)
         objs = []

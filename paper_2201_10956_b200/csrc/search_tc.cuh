@@ -21,11 +21,12 @@ namespace tc {
 constexpr int kJT = 32;                  // j per tile  -> A rows = 4 * 32 = 128
 constexpr int kKT = 64;                  // k per tile  -> B rows = 2 * 64 = 128
 constexpr int kRows = 128;
-constexpr int kChunk = 128;              // samples per smem stage (one word-quad)
-constexpr int kStages = 4;
-constexpr int kStageBytes = 2 * kRows * kChunk;   // A + B = 32 KiB
+constexpr int kChunk = 256;              // samples per smem stage (two word-quads)
+constexpr int kSlabs = kChunk / 16;      // 16-byte K slabs per row per stage
+constexpr int kStages = 3;
+constexpr int kStageBytes = 2 * kRows * kChunk;   // A + B = 64 KiB
 constexpr int kProducerWarps = 8;        // warps 1..8
-constexpr int kEpilogueWarps = 4;        // warps 9..12
+constexpr int kEpilogueWarps = 8;        // warps 9..16: two warpgroups split the k columns
 constexpr int kThreads = 32 * (1 + kProducerWarps + kEpilogueWarps);
 constexpr int kTmemCols = 512;           // 2 buffers x 2 classes x 128 columns
 constexpr uint32_t kIdesc = (2u << 4)                 // D format s32
@@ -42,12 +43,30 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
                : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread is parked by the
+// hardware until the phase completes instead of spinning on issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity), "r"(0x100000)
       : "memory");
+}
+// Waiters that may block for a whole tile back off so their spinning does not
+// steal issue slots from the producer warps on the same SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, ns = 32;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+  }
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -55,7 +74,7 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 // Shared-memory matrix descriptor: K-major, no swizzle, version 1 (sm_100).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
   constexpr uint32_t kLbo = 128;   // next 16-byte K slab
-  constexpr uint32_t kSbo = 1024;  // next 8-row core-matrix group (8 slabs x 128 B)
+  constexpr uint32_t kSbo = kSlabs * 128;  // next 8-row core-matrix group
   return uint64_t((saddr >> 4) & 0x3fff) | (uint64_t(kLbo >> 4) << 16) |
          (uint64_t(kSbo >> 4) << 32) | (uint64_t(1) << 46);
 }
@@ -83,20 +102,19 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // 0x00204081 land on distinct bit positions, so no carries.
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
-// Expands one 128-sample quad (4 words) to 128 bytes in the canonical layout
-// of row r: 16-byte slab s holds samples 16s..16s+15.
-__device__ __forceinline__ void expand_row(uint8_t* stage_base, int r, uint4 q) {
+// Expands one 128-sample quad (4 words) into slabs [8h, 8h+8) of row r in
+// the canonical layout (16-byte slab s holds samples 16s..16s+15 of the stage).
+__device__ __forceinline__ void expand_quad(uint32_t stage_saddr, int r, int h, uint4 q) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-  uint8_t* rowp = stage_base + (r >> 3) * 1024 + (r & 7) * 16;
+  const uint32_t rowa = stage_saddr + (r >> 3) * (kSlabs * 128) + (r & 7) * 16 + h * 8 * 128;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const uint32_t bits = w[s >> 1] >> (16 * (s & 1));
-    uint4 o;
-    o.x = spread4(bits & 0xF);
-    o.y = spread4((bits >> 4) & 0xF);
-    o.z = spread4((bits >> 8) & 0xF);
-    o.w = spread4((bits >> 12) & 0xF);
-    *reinterpret_cast<uint4*>(rowp + s * 128) = o;
+    const uint32_t o0 = spread4(bits & 0xF), o1 = spread4((bits >> 4) & 0xF);
+    const uint32_t o2 = spread4((bits >> 8) & 0xF), o3 = spread4((bits >> 12) & 0xF);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + s * 128), "r"(o0),
+                 "r"(o1), "r"(o2), "r"(o3)
+                 : "memory");
   }
 }
 
@@ -161,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full_bar[s], 32 * kProducerWarps);
+      mbar_init(&full_bar[s], kProducerWarps);
       mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -179,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t nchunks = d.wq[0] + d.wq[1];
+  const uint32_t nch0 = (d.wq[0] + 1) / 2;   // stages of class 0 (two quads each)
+  const uint32_t nchunks = nch0 + (d.wq[1] + 1) / 2;
 
   if (it0 < it1) {
     if (warp == 0) {
@@ -195,14 +214,14 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
             const uint32_t s = n % kStages;
             mbar_wait(&full_bar[s], (n / kStages) & 1);
             fence_after();
-            const uint32_t cls = ch < d.wq[0] ? 0 : 1;
-            const uint32_t first = cls == 0 ? 0 : d.wq[0];
+            const uint32_t cls = ch < nch0 ? 0 : 1;
+            const uint32_t first = cls == 0 ? 0 : nch0;
             const uint32_t dcol = tmem + buf * 256 + cls * 128;
             const uint32_t abase = smem_u32(stages + s * kStageBytes);
             const uint32_t bbase = abase + kRows * kChunk;
 #pragma unroll
             for (int kk = 0; kk < kChunk / 32; ++kk)
-              mma_i8(dcol, smem_desc(abase + kk * 256), smem_desc(bbase + kk * 256),
+              mma_i8(dcol, smem_desc(abase + kk * 256), smem_desc(bbase + kk * 256),  // 2 slabs
                      (ch != first || kk != 0) ? 1u : 0u);
             mma_commit(&empty_bar[s]);
           }
@@ -212,45 +231,74 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
       __syncwarp();
     } else if (warp <= kProducerWarps) {
       // ===================== producers: bits -> bytes =====================
+      // Each thread owns one operand row; the plane words of the next stage
+      // are fetched (not yet combined) while the current stage is expanded.
       const int pt = threadIdx.x - 32;           // 0..255
       const bool is_a = pt < kRows;
       const int r = is_a ? pt : pt - kRows;
-      Walker wk;
-      wk.start(M, a.itemoff, M - 3, it0);
-      uint32_t n = 0;
-      for (uint64_t it = it0; it < it1; ++it) {
-        const uint32_t i = wk.i;
-        uint32_t snp_x, snp_y = 0;
-        int gx, gy = 0;
+      const uint32_t stage0 = smem_u32(stages) + (is_a ? 0 : kRows * kChunk);
+      struct Cursor {
+        Walker wk;
+        uint32_t ch;
+      };
+      struct Words {
+        uint4 x[2], y[2];
+      };
+      Cursor pf;
+      pf.wk.start(M, a.itemoff, M - 3, it0);
+      pf.ch = 0;
+      auto fetch = [&](const Cursor& c, Words& o) {
+        const uint32_t i = c.wk.i;
+        const uint32_t cls = c.ch < nch0 ? 0 : 1;
+        const uint32_t q = 2 * (cls == 0 ? c.ch : c.ch - nch0);
+        const size_t row = size_t(M) * 2;
+        const uint4* pl = (cls ? d.planes[1] : d.planes[0]) + size_t(q) * row;
         if (is_a) {  // row = j_local*4 + a*2 + b
-          snp_x = i;
-          gx = (r >> 1) & 1;
-          snp_y = min(i + 1 + wk.a * kJT + (r >> 2), M - 1);
-          gy = r & 1;
+          const uint32_t j = min(i + 1 + c.wk.a * kJT + (r >> 2), M - 1);
+          const uint32_t xo = 2 * i + ((r >> 1) & 1), yo = 2 * j + (r & 1);
+          o.x[0] = __ldg(pl + xo); o.x[1] = __ldg(pl + row + xo);
+          o.y[0] = __ldg(pl + yo); o.y[1] = __ldg(pl + row + yo);
         } else {     // row = k_local*2 + g
-          snp_x = min(i + 1 + wk.b * kKT + (r >> 1), M - 1);
-          gx = r & 1;
+          const uint32_t k = min(i + 1 + c.wk.b * kKT + (r >> 1), M - 1);
+          const uint32_t xo = 2 * k + (r & 1);
+          o.x[0] = __ldg(pl + xo); o.x[1] = __ldg(pl + row + xo);
         }
-        for (uint32_t ch = 0; ch < nchunks; ++ch, ++n) {
-          const uint32_t s = n % kStages;
-          const uint32_t cls = ch < d.wq[0] ? 0 : 1;
-          const uint32_t q = cls == 0 ? ch : ch - d.wq[0];
-          const uint4* pl = d.planes[cls] + size_t(q) * M * 2;
-          uint4 v = __ldg(pl + 2 * snp_x + gx);
+      };
+      auto advance = [&](Cursor& c) {
+        if (++c.ch == nchunks) {
+          c.ch = 0;
+          c.wk.next();
+        }
+      };
+      const uint64_t total_chunks = (it1 - it0) * nchunks;
+      Words cur, nxt;
+      fetch(pf, cur);
+      advance(pf);
+      for (uint64_t n = 0; n < total_chunks; ++n) {
+        if (n + 1 < total_chunks) {
+          fetch(pf, nxt);
+          advance(pf);
+        }
+        const uint32_t s = uint32_t(n % kStages);
+        mbar_wait(&empty_bar[s], uint32_t((n / kStages) & 1) ^ 1);
+        const uint32_t sb = stage0 + s * kStageBytes;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint4 v = cur.x[h];
           if (is_a) {
-            const uint4 y = __ldg(pl + 2 * snp_y + gy);
-            v.x &= y.x; v.y &= y.y; v.z &= y.z; v.w &= y.w;
+            v.x &= cur.y[h].x; v.y &= cur.y[h].y; v.z &= cur.y[h].z; v.w &= cur.y[h].w;
           }
-          mbar_wait(&empty_bar[s], ((n / kStages) & 1) ^ 1);
-          expand_row(stages + s * kStageBytes + (is_a ? 0 : kRows * kChunk), r, v);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&full_bar[s]);
+          expand_quad(sb, r, h, v);
         }
-        wk.next();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_bar[s]);
+        cur = nxt;
       }
     } else {
       // ===================== epilogue: TMEM -> K2 -> top-k =====================
-      const int ew = warp - 1 - kProducerWarps;      // 0..3
+      const int ew = warp - 1 - kProducerWarps;      // 0..7
+      const int half = ew >> 2;                      // which 32 k's of the tile
       const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
       uint64_t* ls = lists + size_t(ew) * 2 * K;
       uint64_t* lt = ls + K;
@@ -262,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
       uint32_t t = 0;
       for (uint64_t it = it0; it < it1; ++it, ++t) {
         const uint32_t buf = t & 1;
-        mbar_wait(&tfull_bar[buf], (t >> 1) & 1);
+        mbar_wait_sleep(&tfull_bar[buf], (t >> 1) & 1);
         fence_after();
         const uint32_t i = wk.i;
         const uint32_t j = i + 1 + wk.a * kJT + jl;
@@ -278,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
         const uint4 pij1 = __ldg(d.pair[1] + size_t(i) * M + jc);
         const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
         const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
-        for (int m = 0; m < kKT / 4; ++m) {
+        for (int m = half * (kKT / 8); m < (half + 1) * (kKT / 8); ++m) {
           uint32_t v0[8], v1[8];
           const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + buf * 256 + 8 * m;
           tmem_ld8(taddr, v0);
