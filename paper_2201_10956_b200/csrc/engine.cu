@@ -403,6 +403,7 @@ search_kernel(const DevData d, const SearchArgs a) {
 }  // namespace
 
 #include "search_tc.cuh"
+#include "search_syrk.cuh"
 
 namespace {
 
@@ -554,6 +555,16 @@ struct e3_dataset {
   std::vector<uint64_t> h_itemoff;
   uint64_t* itemoff_tc = nullptr;     // tensor-core kernel item prefix (32-j x 64-k tiles)
   std::vector<uint64_t> h_itemoff_tc;
+  std::vector<uint2> h_single[2];     // host copy of the single plane counts
+  // compacted (SYRK) engine scratch, allocated on first use
+  uint4* y_buf = nullptr;
+  size_t y_cap = 0;                   // uint4 elements
+  uint32_t* pos_buf = nullptr;
+  size_t pos_cap = 0;                 // u32 elements
+  syrk::IInfo* info_buf = nullptr;
+  uint64_t* syrk_off = nullptr;
+  size_t info_cap = 0;
+  uint32_t* scratch = nullptr;
   int num_sms = 0, search_ctas_per_sm = 0, search_min_blocks = 1;
   // scratch reused across searches
   ulonglong2* lists[2] = {nullptr, nullptr};
@@ -579,6 +590,11 @@ void release(e3_dataset* ds) {
   cudaFree(ds->logp);
   cudaFree(ds->itemoff);
   cudaFree(ds->itemoff_tc);
+  cudaFree(ds->y_buf);
+  cudaFree(ds->pos_buf);
+  cudaFree(ds->info_buf);
+  cudaFree(ds->syrk_off);
+  cudaFree(ds->scratch);
   cudaFree(ds->gthr);
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
@@ -644,6 +660,11 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     CUDA_TRY(cudaStreamSynchronize(ds->stream));
     CUDA_TRY(cudaFree(raw));
   }
+  for (int c = 0; c < 2; ++c) {
+    ds->h_single[c].resize(M);
+    CUDA_TRY(cudaMemcpyAsync(ds->h_single[c].data(), ds->single[c], sizeof(uint2) * M,
+                             cudaMemcpyDeviceToHost, ds->stream));
+  }
   // K2 log table, built on the host exactly like build_log_table(N+1).
   const uint64_t N = ds->N[0] + ds->N[1];
   std::vector<double> logp(N + 2);
@@ -672,6 +693,12 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(tc::smem_bytes(E3_MAX_TOP_K))));
   CUDA_TRY(cudaFuncSetAttribute(tc::search_tc_kernel<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(tc::smem_bytes(E3_MAX_TOP_K))));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(tc::smem_bytes(E3_MAX_TOP_K))));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(tc::smem_bytes(E3_MAX_TOP_K))));
   CUDA_TRY(cudaMalloc(&ds->gthr, sizeof(uint64_t)));
@@ -754,6 +781,122 @@ extern "C" int e3_dataset_info(const e3_dataset* ds, uint64_t* M, uint64_t* N0, 
 // ---------------------------------------------------------------------------
 // C ABI: search
 // ---------------------------------------------------------------------------
+namespace {
+
+// The compacted tensor-core engine over first-SNP range [i_first, i_last]:
+// batches of i sized to the Y budget, each = positions + gather + SYRK
+// kernel; the per-CTA top-k lists persist across the batches.
+int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_t K, bool ranged,
+             uint32_t i_first, uint32_t i_last, uint32_t grid, uint32_t* launches) {
+  const uint64_t M = ds->M;
+  cudaStream_t st = ds->stream;
+  constexpr size_t kYBudget = size_t(1) << 27;   // uint4 elements (2 GiB)
+  constexpr uint32_t kMaxBatch = 4096;
+  // per-i layout
+  auto layout = [&](uint32_t i, syrk::IInfo& inf, size_t& ysz, size_t& psz) {
+    inf.R = uint32_t(2 * (M - 1 - i));
+    inf.nb = uint32_t((M - 1 - i + syrk::kJB - 1) / syrk::kJB);
+    ysz = 0;
+    psz = 0;
+    for (int a = 0; a < 2; ++a)
+      for (int c = 0; c < 2; ++c) {
+        const uint2 sc = ds->h_single[c][i];
+        inf.n[a][c] = a == 0 ? sc.x : sc.y;
+        inf.q[a][c] = (inf.n[a][c] + 255) / 256 * 2;
+        ysz += size_t(inf.q[a][c]) * inf.R;
+        psz += inf.n[a][c];
+      }
+  };
+  if (!ds->scratch)
+    CUDA_TRY(cudaMalloc(&ds->scratch, sizeof(uint32_t) * size_t(grid) *
+                                          syrk::kScratchPerThread * 256));
+  CUDA_TRY(cudaMemsetAsync(ds->counts[0], 0, sizeof(uint32_t) * grid * tc::kEpilogueWarps, st));
+  std::vector<syrk::IInfo> infos;
+  std::vector<uint64_t> off;
+  uint32_t i = i_first;
+  while (i <= i_last) {
+    infos.clear();
+    off.assign(1, 0);
+    size_t ytot = 0, ptot = 0;
+    uint32_t rmax = 0, qmax = 0;
+    while (i <= i_last && infos.size() < kMaxBatch) {
+      syrk::IInfo inf{};
+      size_t ysz, psz;
+      layout(i, inf, ysz, psz);
+      if (!infos.empty() && ytot + ysz > kYBudget) break;
+      for (int a = 0; a < 2; ++a) {
+        inf.y_off[a] = ytot;
+        ytot += size_t(inf.q[a][0] + inf.q[a][1]) * inf.R;
+        qmax = std::max(qmax, inf.q[a][0] + inf.q[a][1]);
+        for (int c = 0; c < 2; ++c) {
+          inf.pos_off[a][c] = ptot;
+          ptot += inf.n[a][c];
+        }
+      }
+      rmax = std::max(rmax, inf.R);
+      infos.push_back(inf);
+      off.push_back(off.back() + syrk::tiles_of(M, i));
+      ++i;
+    }
+    const uint32_t n_i = uint32_t(infos.size());
+    if (ytot > ds->y_cap) {
+      cudaFree(ds->y_buf);
+      ds->y_buf = nullptr;
+      CUDA_TRY(cudaMalloc(&ds->y_buf, sizeof(uint4) * std::max<size_t>(ytot, 1)));
+      ds->y_cap = ytot;
+    }
+    if (ptot > ds->pos_cap) {
+      cudaFree(ds->pos_buf);
+      ds->pos_buf = nullptr;
+      CUDA_TRY(cudaMalloc(&ds->pos_buf, sizeof(uint32_t) * std::max<size_t>(ptot, 1)));
+      ds->pos_cap = ptot;
+    }
+    if (n_i > ds->info_cap) {
+      cudaFree(ds->info_buf);
+      cudaFree(ds->syrk_off);
+      ds->info_buf = nullptr;
+      ds->syrk_off = nullptr;
+      CUDA_TRY(cudaMalloc(&ds->info_buf, sizeof(syrk::IInfo) * kMaxBatch));
+      CUDA_TRY(cudaMalloc(&ds->syrk_off, sizeof(uint64_t) * (kMaxBatch + 1)));
+      ds->info_cap = kMaxBatch;
+    }
+    // the host vectors are reused next batch: copy synchronously w.r.t. the stream order
+    CUDA_TRY(cudaMemcpyAsync(ds->info_buf, infos.data(), sizeof(syrk::IInfo) * n_i,
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ds->syrk_off, off.data(), sizeof(uint64_t) * (n_i + 1),
+                             cudaMemcpyHostToDevice, st));
+    syrk::SyrkArgs sa{};
+    sa.item_begin = 0;
+    sa.item_count = off.back();
+    sa.rank_begin = r0;
+    sa.rank_end = r1;
+    sa.top_k = K;
+    sa.i_lo = i - n_i;
+    sa.n_i = n_i;
+    sa.gthr = ds->gthr;
+    sa.lists = ds->lists[0];
+    sa.counts = ds->counts[0];
+    sa.info = ds->info_buf;
+    sa.itemoff = ds->syrk_off;
+    sa.Y = ds->y_buf;
+    sa.scratch = ds->scratch;
+    syrk::compact_positions_kernel<<<dim3(n_i, 2, 2), 1024, 0, st>>>(d, sa, ds->pos_buf);
+    if (qmax > 0)
+      syrk::compact_gather_kernel<<<dim3((rmax + 127) / 128, qmax, n_i * 2), 128, 0, st>>>(
+          d, sa, ds->pos_buf, ds->y_buf);
+    const size_t tsm = tc::smem_bytes(K);
+    if (ranged) syrk::search_syrk_kernel<true><<<grid, tc::kThreads, tsm, st>>>(d, sa);
+    else syrk::search_syrk_kernel<false><<<grid, tc::kThreads, tsm, st>>>(d, sa);
+    CUDA_TRY(cudaGetLastError());
+    *launches += 3;
+    // infos/off are rewritten next batch; make sure the async copies consumed them
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return E3_OK;
+}
+
+}  // namespace
+
 extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit* top,
                          uint32_t* n_top, e3_stats* stats) {
   const auto t_start = std::chrono::steady_clock::now();
@@ -786,11 +929,17 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   const bool ranged = !(r0 == 0 && r1 == total);
 
   const uint32_t K = cfg->top_k;
-  // Engine: tensor-core GEMM formulation by default; the POPC kernel on request.
-  const bool use_tc = !(cfg->flags & E3_ENGINE_POPC);
+  // Engines: compacted tensor-core SYRK (default), masked tensor-core GEMM,
+  // LOP3/POPC. All produce identical results.
+  const uint32_t engine = cfg->flags & 3u;
+  const bool use_syrk = engine == 0;
+  const bool use_tc = engine == E3_ENGINE_TC_MASKED;
   uint32_t grid, nlists;
   tc::TcArgs ta{};
-  if (use_tc) {
+  if (use_syrk) {
+    grid = uint32_t(ds->num_sms);
+    nlists = grid * tc::kEpilogueWarps;
+  } else if (use_tc) {
     ta.item_begin = ds->h_itemoff_tc[t0[0]];
     ta.item_count = ds->h_itemoff_tc[t1[0] + 1] - ta.item_begin;
     grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(ds->num_sms, ta.item_count)));
@@ -823,7 +972,11 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   CUDA_TRY(cudaEventRecord(ds->ev[0], st));
   CUDA_TRY(cudaMemsetAsync(ds->gthr, 0xff, sizeof(uint64_t), st));
   CUDA_TRY(cudaEventRecord(ds->ev[1], st));
-  if (use_tc) {
+  uint32_t launches = 1;
+  if (use_syrk) {
+    launches = 0;
+    if (int rc = run_syrk(ds, d, r0, r1, K, ranged, t0[0], t1[0], grid, &launches)) return rc;
+  } else if (use_tc) {
     ta.rank_begin = r0;
     ta.rank_end = r1;
     ta.top_k = K;
@@ -843,7 +996,6 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(ds->ev[2], st));
-  uint32_t launches = 1;
   // Merge rounds: groups of lists -> one list each, until one list remains.
   uint32_t nl = nlists;
   int cur = 0;

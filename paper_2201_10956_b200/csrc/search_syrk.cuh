@@ -1,0 +1,451 @@
+// search_syrk.cuh — compacted tensor-core engine (included by engine.cu after
+// search_tc.cuh; reuses its tcgen05/mbarrier helpers).
+//
+// For a fixed first SNP i and genotype a in {0,1}, the counted cells are a
+// Gram matrix over the samples where SNP i has genotype a:
+//   T_c[a][b][g](i,j,k) = sum_{s in S_{i,a,c}} X_b^j[s] * X_g^k[s],
+//   S_{i,a,c} = { s in class c : X_a^i[s] = 1 }.
+// Compacting the sample axis to S_{i,a,c} (|S_0| + |S_1| ~ 0.91 N at maf 0.3)
+// makes every MMA byte useful: 4 (b,g) MACs per compacted sample instead of
+// the masked formulation's 8 over all samples (2.2x less MMA and operand
+// expansion per triplet x sample). Per batch of i's:
+//   compact_positions_kernel  S_{i,a,c} as sorted in-class positions
+//   compact_gather_kernel     Y_{i,a}[quad][row=(j,b)] = X_b^j at S_{i,a,*}
+//                             (bit-packed, class 0 quads then class 1 quads,
+//                             each class padded to 256 samples)
+//   search_syrk_kernel        tiles (i, 64-j block, 64-k block), j-block <=
+//                             k-block; phase a=0 then a=1 per tile, each into
+//                             its own TMEM buffer (2 classes x 128 columns),
+//                             so the epilogue of one phase overlaps the MMAs
+//                             of the other. The a=0 counts go to a per-CTA
+//                             scratch tile; the a=1 phase completes the 8
+//                             counted cells and runs the exact derivation,
+//                             K2 and top-k of the other engines.
+
+namespace syrk {
+
+using namespace tc;
+
+constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows each
+constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
+constexpr int kScratchPerThread = kRounds * 16;  // u32: 8 values x 2 classes per round
+
+// Per-i layout of the compacted operands (one record per i of the batch).
+struct IInfo {
+  uint64_t y_off[2];     // uint4 offset of Y_{i,a} in the batch buffer
+  uint64_t pos_off[2][2];// u32 offset of S_{i,a,c} in the position buffer
+  uint32_t n[2][2];      // |S_{i,a,c}|
+  uint32_t q[2][2];      // quads of class c in Y_{i,a} (even: 256-sample stages)
+  uint32_t R;            // rows = 2 (M - 1 - i)
+  uint32_t nb;           // 64-SNP blocks above i
+};
+
+struct SyrkArgs {
+  uint64_t item_begin, item_count;   // items of this batch (tile index space)
+  uint64_t rank_begin, rank_end;
+  uint32_t top_k;
+  uint32_t i_lo, n_i;                // batch = [i_lo, i_lo + n_i)
+  uint64_t* gthr;
+  ulonglong2* lists;                 // [grid * kEpilogueWarps][top_k], persistent
+  uint32_t* counts;
+  const IInfo* info;                 // [n_i]
+  const uint64_t* itemoff;           // [n_i + 1] tile prefix within the batch
+  const uint4* Y;
+  uint32_t* scratch;                 // [grid][kRounds * 16][256]
+};
+
+// S_{i,a,c}: block-wide exclusive scan of popcounts over the class words of X_a^i.
+__global__ void __launch_bounds__(1024) compact_positions_kernel(const DevData d, SyrkArgs s,
+                                                                uint32_t* __restrict__ pos) {
+  const uint32_t ii = blockIdx.x, a = blockIdx.y, c = blockIdx.z;
+  const uint32_t i = s.i_lo + ii;
+  const IInfo inf = s.info[ii];
+  uint32_t* out = pos + inf.pos_off[a][c];
+  const uint32_t nw = d.wq[c] * 4;
+  const uint4* pl = c ? d.planes[1] : d.planes[0];
+  const size_t row = size_t(d.M) * 2;
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t w0 = 0; w0 < nw; w0 += blockDim.x) {
+    const uint32_t w = w0 + threadIdx.x;
+    uint32_t bits = 0;
+    if (w < nw) {
+      const uint4 q = __ldg(pl + size_t(w >> 2) * row + 2 * i + a);
+      const uint32_t comp[4] = {q.x, q.y, q.z, q.w};
+      bits = comp[w & 3];
+    }
+    const uint32_t cnt = __popc(bits);
+    // block exclusive scan of cnt
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((threadIdx.x & 31) >= o) incl += v;
+    }
+    if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t t = threadIdx.x < (blockDim.x >> 5) ? warp_tot[threadIdx.x] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, t, o);
+        if (threadIdx.x >= o) t += v;
+      }
+      warp_tot[threadIdx.x] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t wid = threadIdx.x >> 5;
+    uint32_t off = carry + incl - cnt + (wid ? warp_tot[wid - 1] : 0);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      out[off++] = w * 32 + b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+}
+
+// Y_{i,a}[q][row] = 128 compacted sample bits of row (j, b), j = i+1+row/2.
+__global__ void __launch_bounds__(128) compact_gather_kernel(const DevData d, SyrkArgs s,
+                                                             const uint32_t* __restrict__ pos,
+                                                             uint4* __restrict__ Y) {
+  const uint32_t ii = blockIdx.z >> 1, a = blockIdx.z & 1;
+  const IInfo inf = s.info[ii];
+  const uint32_t qtot = inf.q[a][0] + inf.q[a][1];
+  const uint32_t q = blockIdx.y;
+  if (q >= qtot) return;
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= inf.R) return;
+  const uint32_t i = s.i_lo + ii;
+  const uint32_t c = q < inf.q[a][0] ? 0 : 1;
+  const uint32_t ql = c ? q - inf.q[a][0] : q;
+  const uint32_t n = inf.n[a][c];
+  const uint32_t* P = pos + inf.pos_off[a][c];
+  const uint32_t snp = i + 1 + (row >> 1), g = row & 1;
+  const uint4* pl = (c ? d.planes[1] : d.planes[0]) + 2 * snp + g;
+  const size_t qrow = size_t(d.M) * 2;
+  uint32_t outw[4] = {0, 0, 0, 0};
+  uint32_t cur_q = 0xffffffffu;
+  uint4 cq = make_uint4(0, 0, 0, 0);
+  const uint32_t base = ql * 128;
+  for (uint32_t t = 0; t < 128; ++t) {
+    const uint32_t idx = base + t;
+    if (idx >= n) break;
+    const uint32_t p = __ldg(P + idx);
+    const uint32_t pq = p >> 7;
+    if (pq != cur_q) {
+      cq = __ldg(pl + size_t(pq) * qrow);
+      cur_q = pq;
+    }
+    const uint32_t w = (p >> 5) & 3;
+    const uint32_t word = w == 0 ? cq.x : (w == 1 ? cq.y : (w == 2 ? cq.z : cq.w));
+    outw[t >> 5] |= ((word >> (p & 31)) & 1u) << (t & 31);
+  }
+  Y[inf.y_off[a] + size_t(q) * inf.R + row] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+}
+
+// Tile walk within a batch: (i, jb, kb) with jb <= kb < nb(i).
+struct SWalker {
+  uint32_t ii, jb, kb, nb;
+  __device__ void start(const SyrkArgs& s, uint64_t item) {
+    uint32_t lo = 0, hi = s.n_i - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (s.itemoff[mid] <= item) lo = mid; else hi = mid - 1;
+    }
+    ii = lo;
+    nb = s.info[ii].nb;
+    uint64_t u = item - s.itemoff[ii];
+    jb = 0;
+    while (u >= uint64_t(nb - jb)) { u -= nb - jb; ++jb; }
+    kb = jb + uint32_t(u);
+  }
+  __device__ void next(const SyrkArgs& s) {
+    if (++kb == nb) {
+      if (++jb == nb) {
+        ++ii;
+        jb = 0;
+        if (ii < s.n_i) nb = s.info[ii].nb;
+      }
+      kb = jb;
+    }
+  }
+};
+
+template <bool kRanged>
+__global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t M = d.M;
+  const uint32_t K = s.top_k;
+  const uint64_t it0 = s.item_begin + s.item_count * blockIdx.x / gridDim.x;
+  const uint64_t it1 = s.item_begin + s.item_count * (blockIdx.x + 1) / gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full_bar[st], kProducerWarps);
+      mbar_init(&empty_bar[st], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 32 * kEpilogueWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)), "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0 && it0 < it1) {
+      SWalker wk;
+      wk.start(s, it0);
+      uint32_t n = 0;
+      for (uint64_t it = it0; it < it1; ++it) {
+        const IInfo& inf = s.info[wk.ii];
+#pragma unroll
+        for (uint32_t a = 0; a < 2; ++a) {
+          const uint32_t t2 = uint32_t(it - it0);  // phase a of tile t uses buffer a
+          mbar_wait(&tempty_bar[a], (t2 & 1) ^ 1);
+          fence_after();
+#pragma unroll
+          for (uint32_t c = 0; c < 2; ++c) {
+            const uint32_t nch = inf.q[a][c] / 2;
+            const uint32_t dcol = tmem + a * 256 + c * 128;
+            for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
+              const uint32_t st = n % kStages;
+              mbar_wait(&full_bar[st], (n / kStages) & 1);
+              fence_after();
+              const uint32_t abase = smem_u32(stages + st * kStageBytes);
+              const uint32_t bbase = abase + kRows * kChunk;
+#pragma unroll
+              for (int kk = 0; kk < kChunk / 32; ++kk)
+                mma_i8(dcol, smem_desc(abase + kk * 256), smem_desc(bbase + kk * 256),
+                       (ch != 0 || kk != 0) ? 1u : 0u);
+              mma_commit(&empty_bar[st]);
+            }
+          }
+          mma_commit(&tfull_bar[a]);
+        }
+        wk.next(s);
+      }
+    }
+    __syncwarp();
+  } else if (warp <= kProducerWarps) {
+    // ===================== producers: compacted bits -> bytes =====================
+    const int pt = threadIdx.x - 32;
+    const bool is_a = pt < kRows;
+    const int r = is_a ? pt : pt - kRows;
+    const uint32_t stage0 = smem_u32(stages) + (is_a ? 0 : kRows * kChunk);
+    if (it0 < it1) {
+      SWalker wk;
+      wk.start(s, it0);
+      uint32_t n = 0;
+      uint32_t st = 0, ph = 0;
+      for (uint64_t it = it0; it < it1; ++it) {
+        const IInfo inf = s.info[wk.ii];
+        const uint32_t rowi = min((is_a ? wk.jb : wk.kb) * 2 * kJB + r, inf.R - 1);
+#pragma unroll
+        for (uint32_t a = 0; a < 2; ++a) {
+          const uint4* Ya = s.Y + inf.y_off[a] + rowi;
+          const uint32_t qtot = inf.q[a][0] + inf.q[a][1];
+          // stages walk the quads of class 0 then class 1 (both even counts)
+          uint4 c0, c1;
+          if (qtot) {
+            c0 = __ldg(Ya);
+            c1 = __ldg(Ya + size_t(inf.R));
+          }
+          for (uint32_t q = 0; q < qtot; q += 2, ++n) {
+            uint4 n0 = c0, n1 = c1;
+            if (q + 2 < qtot) {
+              n0 = __ldg(Ya + size_t(q + 2) * inf.R);
+              n1 = __ldg(Ya + size_t(q + 3) * inf.R);
+            }
+            mbar_wait(&empty_bar[st], ph ^ 1);
+            const uint32_t sb = stage0 + st * kStageBytes;
+            expand_quad(sb, r, 0, c0);
+            expand_quad(sb, r, 1, c1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full_bar[st]);
+            if (++st == kStages) { st = 0; ph ^= 1; }
+            c0 = n0;
+            c1 = n1;
+          }
+        }
+        wk.next(s);
+      }
+      (void)n;
+    }
+  } else {
+    // ===================== epilogue =====================
+    const int ew = warp - 1 - kProducerWarps;   // 0..7
+    const int half = ew >> 2;                   // k columns [32*half, 32*half+32)
+    const int quarter = warp & 3;               // TMEM lane quarter
+    const int et = ew * 32 + lane;              // 0..255 scratch slot
+    uint64_t* ls = lists + size_t(ew) * 2 * K;
+    uint64_t* lt = ls + K;
+    const size_t list = size_t(blockIdx.x) * kEpilogueWarps + ew;
+    uint32_t nlist = s.counts[list];
+    for (uint32_t e = lane; e < nlist; e += 32) {
+      const ulonglong2 v = s.lists[list * K + e];
+      ls[e] = v.x;
+      lt[e] = v.y;
+    }
+    __syncwarp();
+    const int jl = quarter * 16 + (lane >> 1);  // row = 2*j_local + b
+    const int bsel = lane & 1;
+    uint32_t* scr = s.scratch + size_t(blockIdx.x) * kScratchPerThread * 256 + et;
+    if (it0 < it1) {
+      SWalker wk;
+      wk.start(s, it0);
+      for (uint64_t it = it0; it < it1; ++it) {
+        const uint32_t t2 = uint32_t(it - it0);
+        const IInfo inf = s.info[wk.ii];
+        const uint32_t i = s.i_lo + wk.ii;
+        // ---- phase a = 0: TMEM -> scratch
+        mbar_wait_sleep(&tfull_bar[0], t2 & 1);
+        fence_after();
+        for (int m = 0; m < kRounds; ++m) {
+          uint32_t v0[8], v1[8];
+          const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + 8 * (half * kRounds + m);
+          tmem_ld8(taddr, v0);
+          tmem_ld8(taddr + 128, v1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            scr[(m * 16 + x) * 256] = inf.q[0][0] ? v0[x] : 0u;
+            scr[(m * 16 + 8 + x) * 256] = inf.q[0][1] ? v1[x] : 0u;
+          }
+        }
+        fence_before();
+        mbar_arrive(&tempty_bar[0]);
+        // ---- phase a = 1: TMEM + scratch -> cells -> K2 -> top-k
+        mbar_wait_sleep(&tfull_bar[1], t2 & 1);
+        fence_after();
+        const uint32_t j = i + 1 + wk.jb * kJB + jl;
+        const uint32_t jc = min(j, M - 1);
+        const uint64_t gth = *reinterpret_cast<volatile uint64_t*>(s.gthr);
+        uint64_t rank_ij = 0;
+        if (kRanged) {
+          const uint64_t Mi = M - i, Mj = M - jc;
+          rank_ij = (uint64_t(M) * (M - 1) * (M - 2) - Mi * (Mi - 1) * (Mi - 2)) / 6 +
+                    (uint64_t(Mi - 1) * (Mi - 2)) / 2 - Mj * (Mj - 1) / 2;
+        }
+        const uint4 pij0 = __ldg(d.pair[0] + size_t(i) * M + jc);
+        const uint4 pij1 = __ldg(d.pair[1] + size_t(i) * M + jc);
+        const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
+        const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
+        for (int m = 0; m < kRounds; ++m) {
+          uint32_t v0[8], v1[8], u0[8], u1[8];
+          const uint32_t taddr =
+              tmem + (uint32_t(quarter * 32) << 16) + 256 + 8 * (half * kRounds + m);
+          tmem_ld8(taddr, v0);
+          tmem_ld8(taddr + 128, v1);
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            u0[x] = scr[(m * 16 + x) * 256];
+            u1[x] = scr[(m * 16 + 8 + x) * 256];
+          }
+          tmem_wait_ld();
+          if (inf.q[1][0] == 0) for (int x = 0; x < 8; ++x) v0[x] = 0;
+          if (inf.q[1][1] == 0) for (int x = 0; x < 8; ++x) v1[x] = 0;
+          // This thread holds T_a[b=bsel][g] for k phases t=0..3 (index 2t+g),
+          // a=0 in u (scratch), a=1 in v (TMEM). Thread b owns phases 2b, 2b+1;
+          // it sends the partner (b^1) its values for the partner's phases.
+          uint32_t snd[16], rcv[16];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int h = x >> 1, g = x & 1;
+            const int i_b0 = 2 * (2 + h) + g;  // partner phases when bsel == 0: 2, 3
+            const int i_b1 = 2 * h + g;        // partner phases when bsel == 1: 0, 1
+            snd[x] = bsel ? u0[i_b1] : u0[i_b0];
+            snd[4 + x] = bsel ? u1[i_b1] : u1[i_b0];
+            snd[8 + x] = bsel ? v0[i_b1] : v0[i_b0];
+            snd[12 + x] = bsel ? v1[i_b1] : v1[i_b0];
+          }
+#pragma unroll
+          for (int x = 0; x < 16; ++x) rcv[x] = __shfl_xor_sync(0xffffffffu, snd[x], 1);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // the two k phases this thread owns
+            const int tt = 2 * bsel + h;
+            uint32_t T0[8], T1[8];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              const int o0 = 2 * h + g, o1 = 2 * (2 + h) + g;  // own index for bsel 0 / 1
+              const uint32_t own_u0 = bsel ? u0[o1] : u0[o0], own_u1 = bsel ? u1[o1] : u1[o0];
+              const uint32_t own_v0 = bsel ? v0[o1] : v0[o0], own_v1 = bsel ? v1[o1] : v1[o0];
+              const int px = h * 2 + g;
+#pragma unroll
+              for (int bb = 0; bb < 2; ++bb) {
+                const bool mine = bb == bsel;
+                T0[0 * 4 + bb * 2 + g] = mine ? own_u0 : rcv[px];
+                T1[0 * 4 + bb * 2 + g] = mine ? own_u1 : rcv[4 + px];
+                T0[1 * 4 + bb * 2 + g] = mine ? own_v0 : rcv[8 + px];
+                T1[1 * 4 + bb * 2 + g] = mine ? own_v1 : rcv[12 + px];
+              }
+            }
+            const uint32_t k = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + tt;
+            const uint32_t kc = min(k, M - 1);
+            bool valid = j < k && k < M;
+            if (kRanged && valid) {
+              const uint64_t rr = rank_ij + (k - j - 1);
+              valid = rr >= s.rank_begin && rr < s.rank_end;
+            }
+            uint64_t sk = ~0ull, tk = ~0ull;
+            if (valid) {
+              uint32_t n0[27], n1[27];
+              derive_cells(T0, pij0, __ldg(d.pair[0] + size_t(i) * M + kc),
+                           __ldg(d.pair[0] + size_t(jc) * M + kc), si0, sj0,
+                           __ldg(d.single[0] + kc), d.n[0], n0);
+              derive_cells(T1, pij1, __ldg(d.pair[1] + size_t(i) * M + kc),
+                           __ldg(d.pair[1] + size_t(jc) * M + kc), si1, sj1,
+                           __ldg(d.single[1] + kc), d.n[1], n1);
+              sk = score_key(k2_device(n0, n1, d.logp));
+              tk = triple_key(i, j, k);
+            }
+            const bool want = valid && sk <= gth &&
+                              (nlist < K || key_less(sk, tk, ls[K - 1], lt[K - 1]));
+            const unsigned cand = __ballot_sync(0xffffffffu, want);
+            if (cand) warp_insert(ls, lt, nlist, K, cand, sk, tk, lane, s.gthr);
+          }
+        }
+        fence_before();
+        mbar_arrive(&tempty_bar[1]);
+        wk.next(s);
+      }
+    }
+    for (uint32_t e = lane; e < nlist; e += 32) s.lists[list * K + e] = make_ulonglong2(ls[e], lt[e]);
+    if (lane == 0) s.counts[list] = nlist;
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  }
+}
+
+inline uint64_t tiles_of(uint64_t M, uint64_t i) {
+  const uint64_t nb = (M - 1 - i + kJB - 1) / kJB;
+  return nb * (nb + 1) / 2;
+}
+
+}  // namespace syrk

@@ -95,7 +95,9 @@ class e3_plant(C.Structure):
 
 
 MAX_TOP_K = 256
-ENGINES = {"tc": 0, "popc": 1}  # e3_search_cfg.flags (E3_ENGINE_POPC = 1)
+# e3_search_cfg.flags: 0 = compacted tensor-core SYRK (default),
+# E3_ENGINE_POPC = 1, E3_ENGINE_TC_MASKED = 2
+ENGINES = {"syrk": 0, "popc": 1, "tc_masked": 2}
 _P = C.c_void_p
 _U64 = C.c_uint64
 _U32 = C.c_uint32
@@ -329,7 +331,7 @@ class SearchConfig:
     top_k: int = 10
     rank_begin: int = 0
     rank_end: int = 0  # 0 = C(M,3)
-    engine: str = "tc"  # "tc": tcgen05 kind::i8 GEMM kernel; "popc": LOP3/POPC kernel
+    engine: str = "syrk"  # "syrk" (default) | "tc_masked" | "popc" — identical results
 
 
 def same_outcome(a: SearchResult, b: SearchResult) -> bool:

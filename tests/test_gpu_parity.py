@@ -55,7 +55,7 @@ def test_all_tables_and_scores_vs_oracle(M, n0, n1, seed):
         assert float(s).hex() == po.k2_score(expect, P).hex(), t
 
 
-@pytest.mark.parametrize("engine", ["tc", "popc"])
+@pytest.mark.parametrize("engine", ["syrk", "tc_masked", "popc"])
 def test_search_matches_reference_golden(golden, engine):
     for case in golden["cases"]:
         expect = ref_hits(case["search"])
@@ -83,7 +83,7 @@ def test_planted_recovery(golden):
     assert hit >= 19
 
 
-@pytest.mark.parametrize("engine", ["tc", "popc"])
+@pytest.mark.parametrize("engine", ["syrk", "tc_masked", "popc"])
 @pytest.mark.parametrize("top_k", [1, 2, 17, 100, 256])
 def test_top_k_sizes_vs_oracle(top_k, engine):
     ds = _random_ds(40, 300, 211, 11)
@@ -93,7 +93,7 @@ def test_top_k_sizes_vs_oracle(top_k, engine):
     assert res.top[0] == res.best
 
 
-@pytest.mark.parametrize("engine", ["tc", "popc"])
+@pytest.mark.parametrize("engine", ["syrk", "tc_masked", "popc"])
 def test_ranged_searches_vs_oracle(engine):
     ds = _random_ds(90, 700, 300, 12)
     od = po.OracleDataset.of(ds)
@@ -107,7 +107,7 @@ def test_ranged_searches_vs_oracle(engine):
             assert_hits_identical(hits_of(res), od.search(top_k=7, r0=a, r1=b))
 
 
-@pytest.mark.parametrize("engine", ["tc", "popc"])
+@pytest.mark.parametrize("engine", ["syrk", "tc_masked", "popc"])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_partition_then_merge_equals_whole(G, engine):
     # the multi-GPU contract: equal-work ranges searched independently and
@@ -160,7 +160,7 @@ def _config_dataset(M, N, n1, seed):
     return epi3.binarize(geno, pheno), plant.triple
 
 
-@pytest.mark.parametrize("engine", ["tc", "popc"])
+@pytest.mark.parametrize("engine", ["syrk", "tc_masked", "popc"])
 @pytest.mark.parametrize("name,M,N,n1,top_k,ranges", [
     ("cfg3", 8192, 16384, 8192, 10, 3),
     ("cfg4", 1024, 262144, 131072, 10, 2),
@@ -194,6 +194,7 @@ def test_engines_agree_on_random_inputs():
         n0, n1 = int(rng.integers(0, 700)), int(rng.integers(1, 700))
         ds = _random_ds(M, n0, n1, 100 + rep)
         with epi3.DeviceDataset(ds) as dd:
-            a = dd.search(epi3.SearchConfig(top_k=33, engine="tc"))
+            a = dd.search(epi3.SearchConfig(top_k=33, engine="syrk"))
             b = dd.search(epi3.SearchConfig(top_k=33, engine="popc"))
-        assert epi3.same_outcome(a, b), (M, n0, n1)
+            c = dd.search(epi3.SearchConfig(top_k=33, engine="tc_masked"))
+        assert epi3.same_outcome(a, b) and epi3.same_outcome(a, c), (M, n0, n1)
