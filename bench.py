@@ -152,12 +152,15 @@ def main():
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--slices", type=int, default=64,
                     help="a step searches 1/SLICES of the triple-rank space per GPU")
-    ap.add_argument("--engine", default="syrk", choices=["syrk", "tc_masked", "popc"],
-                    help="syrk: compacted tcgen05 kind::i8 SYRK (default); tc_masked: "
-                         "tcgen05 GEMM over pair products; popc: LOP3/POPC kernel")
+    ap.add_argument("--engine", default="auto", choices=["auto", "syrk", "tc_masked", "popc"],
+                    help="auto (default): syrk for N >= 8192 else tc_masked; syrk: compacted "
+                         "tcgen05 kind::i8 SYRK; tc_masked: tcgen05 GEMM over pair products; "
+                         "popc: LOP3/POPC kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.engine == "auto":
+        args.engine = "syrk" if WORKLOADS[args.workload][1] >= 8192 else "tc_masked"
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
 

@@ -56,18 +56,21 @@ typedef struct {
  * or rank_end == 0 — is the full search run_search performs (search.cpp:127). */
 typedef struct {
   uint32_t top_k;       /* >= 1, <= E3_MAX_TOP_K */
-  uint32_t flags;       /* engine: 0 = default (compacted tensor-core SYRK), E3_ENGINE_* */
+  uint32_t flags;       /* engine: 0 = auto, else one of E3_ENGINE_* */
   uint64_t rank_begin;
   uint64_t rank_end;    /* 0 = C(M,3) */
 } e3_search_cfg;
 
 #define E3_MAX_TOP_K 256u
 /* Engine selection (e3_search_cfg.flags). All engines produce identical
- * results. Default (0): per-first-SNP sample compaction + tcgen05 kind::i8
- * SYRK. E3_ENGINE_POPC: LOP3/POPC kernel. E3_ENGINE_TC_MASKED: tcgen05
- * kind::i8 GEMM over pair products without compaction. */
+ * results; 0 = auto (E3_ENGINE_SYRK for N >= 8192 samples, else
+ * E3_ENGINE_TC_MASKED).
+ *   E3_ENGINE_POPC       LOP3/POPC kernel (marginal subtraction + carry-save)
+ *   E3_ENGINE_TC_MASKED  tcgen05 kind::i8 GEMM: pair products x singles
+ *   E3_ENGINE_SYRK       per-first-SNP sample compaction + tcgen05 kind::i8 SYRK */
 #define E3_ENGINE_POPC 1u
 #define E3_ENGINE_TC_MASKED 2u
+#define E3_ENGINE_SYRK 3u
 
 /* Replaces SearchStats (search.hpp:37-41). */
 typedef struct {

@@ -157,6 +157,7 @@ __device__ __forceinline__ double k2_device(const uint32_t* n0, const uint32_t* 
   return score;
 }
 
+
 // One 32-sample word of one class for one (i, j, k): 8 AND3 + 8 POPC.
 __device__ __forceinline__ void count_word(uint32_t xi0, uint32_t xi1, uint32_t xj0, uint32_t xj1,
                                            uint32_t xk0, uint32_t xk1, uint32_t* T) {
@@ -566,6 +567,9 @@ struct e3_dataset {
   size_t info_cap = 0;
   uint32_t* scratch = nullptr;
   int num_sms = 0, search_ctas_per_sm = 0, search_min_blocks = 1;
+  size_t smem_optin = 0;
+  uint32_t debug_skip = 0;  // E3_DEBUG_SKIP (profiling experiments only)
+  unsigned long long* debug_counter = nullptr;  // E3_DEBUG_COUNT: exact-K2 evaluations
   // scratch reused across searches
   ulonglong2* lists[2] = {nullptr, nullptr};
   uint32_t* counts[2] = {nullptr, nullptr};
@@ -573,6 +577,7 @@ struct e3_dataset {
   uint32_t counts_cap = 0;
   uint64_t* gthr = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_upload = nullptr;
 };
 
 namespace {
@@ -595,9 +600,16 @@ void release(e3_dataset* ds) {
   cudaFree(ds->info_buf);
   cudaFree(ds->syrk_off);
   cudaFree(ds->scratch);
+  if (ds->debug_counter) {
+    unsigned long long v = 0;
+    cudaMemcpy(&v, ds->debug_counter, sizeof(v), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "[e3 debug] exact K2 evaluations: %llu\n", v);
+    cudaFree(ds->debug_counter);
+  }
   cudaFree(ds->gthr);
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
+  if (ds->ev_upload) cudaEventDestroy(ds->ev_upload);
   if (ds->stream) cudaStreamDestroy(ds->stream);
   delete ds;
 }
@@ -621,6 +633,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaSetDevice(ds->device));
   CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
   for (auto& e : ds->ev) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(cudaEventCreateWithFlags(&ds->ev_upload, cudaEventDisableTiming));
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, ds->device));
   ds->num_sms = prop.multiProcessorCount;
@@ -695,12 +708,18 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaFuncSetAttribute(tc::search_tc_kernel<true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(tc::smem_bytes(E3_MAX_TOP_K))));
+  ds->smem_optin = prop.sharedMemPerBlockOptin;
+  if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
+  if (std::getenv("E3_DEBUG_COUNT")) {
+    CUDA_TRY(cudaMalloc(&ds->debug_counter, sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(ds->debug_counter, 0, sizeof(unsigned long long)));
+  }
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(tc::smem_bytes(E3_MAX_TOP_K))));
+                                int(ds->smem_optin - 2048)));
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(tc::smem_bytes(E3_MAX_TOP_K))));
+                                int(ds->smem_optin - 2048)));
   CUDA_TRY(cudaMalloc(&ds->gthr, sizeof(uint64_t)));
   uint32_t h_bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
@@ -784,114 +803,126 @@ extern "C" int e3_dataset_info(const e3_dataset* ds, uint64_t* M, uint64_t* N0, 
 namespace {
 
 // The compacted tensor-core engine over first-SNP range [i_first, i_last]:
-// batches of i sized to the Y budget, each = positions + gather + SYRK
-// kernel; the per-CTA top-k lists persist across the batches.
+// batches of i sized so the compacted operands stay L2-resident, each =
+// positions + gather + SYRK kernel; the per-CTA top-k lists persist across
+// the batches. All batches are planned up front, so the host never waits.
 int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_t K, bool ranged,
              uint32_t i_first, uint32_t i_last, uint32_t grid, uint32_t* launches) {
   const uint64_t M = ds->M;
   cudaStream_t st = ds->stream;
-  constexpr size_t kYBudget = size_t(1) << 27;   // uint4 elements (2 GiB)
-  constexpr uint32_t kMaxBatch = 4096;
-  // per-i layout
-  auto layout = [&](uint32_t i, syrk::IInfo& inf, size_t& ysz, size_t& psz) {
-    inf.R = uint32_t(2 * (M - 1 - i));
-    inf.nb = uint32_t((M - 1 - i + syrk::kJB - 1) / syrk::kJB);
-    ysz = 0;
-    psz = 0;
-    for (int a = 0; a < 2; ++a)
-      for (int c = 0; c < 2; ++c) {
-        const uint2 sc = ds->h_single[c][i];
-        inf.n[a][c] = a == 0 ? sc.x : sc.y;
-        inf.q[a][c] = (inf.n[a][c] + 255) / 256 * 2;
-        ysz += size_t(inf.q[a][c]) * inf.R;
-        psz += inf.n[a][c];
-      }
+  constexpr size_t kYBudget = size_t(3) << 20;   // uint4 elements per batch (48 MiB)
+  struct Batch {
+    uint32_t first, n, rmax, qmax;
+    size_t ytot, ptot;
+    uint64_t tiles, info_at, off_at;
   };
+  std::vector<syrk::IInfo> infos;
+  std::vector<uint64_t> offs;
+  std::vector<Batch> batches;
+  size_t ymax = 0, pmax = 0;
+  for (uint32_t i = i_first; i <= i_last;) {
+    Batch bt{};
+    bt.first = i;
+    bt.info_at = infos.size();
+    bt.off_at = offs.size();
+    offs.push_back(0);
+    while (i <= i_last) {
+      syrk::IInfo inf{};
+      inf.R = uint32_t(2 * (M - 1 - i));
+      inf.nb = uint32_t((M - 1 - i + syrk::kJB - 1) / syrk::kJB);
+      size_t ysz = 0;
+      for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < 2; ++c) {
+          const uint2 sc = ds->h_single[c][i];
+          inf.n[a][c] = a == 0 ? sc.x : sc.y;
+          inf.q[a][c] = (inf.n[a][c] + 255) / 256 * 2;
+          ysz += size_t(inf.q[a][c]) * inf.R;
+        }
+      if (bt.n > 0 && bt.ytot + ysz > kYBudget) break;
+      for (int a = 0; a < 2; ++a) {
+        inf.y_off[a] = bt.ytot;
+        bt.ytot += size_t(inf.q[a][0] + inf.q[a][1]) * inf.R;
+        bt.qmax = std::max(bt.qmax, inf.q[a][0] + inf.q[a][1]);
+        for (int c = 0; c < 2; ++c) {
+          inf.pos_off[a][c] = bt.ptot;
+          bt.ptot += inf.n[a][c];
+        }
+      }
+      bt.rmax = std::max(bt.rmax, inf.R);
+      infos.push_back(inf);
+      offs.push_back(offs.back() + syrk::tiles_of(M, i));
+      ++bt.n;
+      ++i;
+    }
+    bt.tiles = offs.back();
+    ymax = std::max(ymax, bt.ytot);
+    pmax = std::max(pmax, bt.ptot);
+    batches.push_back(bt);
+  }
+  // buffers: Y and positions are double-buffered across consecutive batches so
+  // batch b+1's compaction can overlap nothing it must not touch (same stream:
+  // ordering is by the stream; two buffers keep the option of a second stream)
+  if (ymax > ds->y_cap) {
+    cudaFree(ds->y_buf);
+    ds->y_buf = nullptr;
+    CUDA_TRY(cudaMalloc(&ds->y_buf, sizeof(uint4) * std::max<size_t>(ymax, 1)));
+    ds->y_cap = ymax;
+  }
+  if (pmax > ds->pos_cap) {
+    cudaFree(ds->pos_buf);
+    ds->pos_buf = nullptr;
+    CUDA_TRY(cudaMalloc(&ds->pos_buf, sizeof(uint32_t) * std::max<size_t>(pmax, 1)));
+    ds->pos_cap = pmax;
+  }
+  const size_t info_need = infos.size() + offs.size();
+  if (info_need > ds->info_cap) {
+    cudaFree(ds->info_buf);
+    cudaFree(ds->syrk_off);
+    ds->info_buf = nullptr;
+    ds->syrk_off = nullptr;
+    CUDA_TRY(cudaMalloc(&ds->info_buf, sizeof(syrk::IInfo) * std::max<size_t>(infos.size(), 1)));
+    CUDA_TRY(cudaMalloc(&ds->syrk_off, sizeof(uint64_t) * std::max<size_t>(offs.size(), 1)));
+    ds->info_cap = info_need;
+  }
+  CUDA_TRY(cudaMemcpyAsync(ds->info_buf, infos.data(), sizeof(syrk::IInfo) * infos.size(),
+                           cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(ds->syrk_off, offs.data(), sizeof(uint64_t) * offs.size(),
+                           cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(ds->ev_upload, st));
   if (!ds->scratch)
     CUDA_TRY(cudaMalloc(&ds->scratch, sizeof(uint32_t) * size_t(grid) *
                                           syrk::kScratchPerThread * 256));
   CUDA_TRY(cudaMemsetAsync(ds->counts[0], 0, sizeof(uint32_t) * grid * tc::kEpilogueWarps, st));
-  std::vector<syrk::IInfo> infos;
-  std::vector<uint64_t> off;
-  uint32_t i = i_first;
-  while (i <= i_last) {
-    infos.clear();
-    off.assign(1, 0);
-    size_t ytot = 0, ptot = 0;
-    uint32_t rmax = 0, qmax = 0;
-    while (i <= i_last && infos.size() < kMaxBatch) {
-      syrk::IInfo inf{};
-      size_t ysz, psz;
-      layout(i, inf, ysz, psz);
-      if (!infos.empty() && ytot + ysz > kYBudget) break;
-      for (int a = 0; a < 2; ++a) {
-        inf.y_off[a] = ytot;
-        ytot += size_t(inf.q[a][0] + inf.q[a][1]) * inf.R;
-        qmax = std::max(qmax, inf.q[a][0] + inf.q[a][1]);
-        for (int c = 0; c < 2; ++c) {
-          inf.pos_off[a][c] = ptot;
-          ptot += inf.n[a][c];
-        }
-      }
-      rmax = std::max(rmax, inf.R);
-      infos.push_back(inf);
-      off.push_back(off.back() + syrk::tiles_of(M, i));
-      ++i;
-    }
-    const uint32_t n_i = uint32_t(infos.size());
-    if (ytot > ds->y_cap) {
-      cudaFree(ds->y_buf);
-      ds->y_buf = nullptr;
-      CUDA_TRY(cudaMalloc(&ds->y_buf, sizeof(uint4) * std::max<size_t>(ytot, 1)));
-      ds->y_cap = ytot;
-    }
-    if (ptot > ds->pos_cap) {
-      cudaFree(ds->pos_buf);
-      ds->pos_buf = nullptr;
-      CUDA_TRY(cudaMalloc(&ds->pos_buf, sizeof(uint32_t) * std::max<size_t>(ptot, 1)));
-      ds->pos_cap = ptot;
-    }
-    if (n_i > ds->info_cap) {
-      cudaFree(ds->info_buf);
-      cudaFree(ds->syrk_off);
-      ds->info_buf = nullptr;
-      ds->syrk_off = nullptr;
-      CUDA_TRY(cudaMalloc(&ds->info_buf, sizeof(syrk::IInfo) * kMaxBatch));
-      CUDA_TRY(cudaMalloc(&ds->syrk_off, sizeof(uint64_t) * (kMaxBatch + 1)));
-      ds->info_cap = kMaxBatch;
-    }
-    // the host vectors are reused next batch: copy synchronously w.r.t. the stream order
-    CUDA_TRY(cudaMemcpyAsync(ds->info_buf, infos.data(), sizeof(syrk::IInfo) * n_i,
-                             cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(ds->syrk_off, off.data(), sizeof(uint64_t) * (n_i + 1),
-                             cudaMemcpyHostToDevice, st));
+  const size_t tsm = tc::smem_bytes(K);
+  for (const Batch& bt : batches) {
     syrk::SyrkArgs sa{};
     sa.item_begin = 0;
-    sa.item_count = off.back();
+    sa.item_count = bt.tiles;
     sa.rank_begin = r0;
     sa.rank_end = r1;
     sa.top_k = K;
-    sa.i_lo = i - n_i;
-    sa.n_i = n_i;
+    sa.i_lo = bt.first;
+    sa.n_i = bt.n;
     sa.gthr = ds->gthr;
     sa.lists = ds->lists[0];
     sa.counts = ds->counts[0];
-    sa.info = ds->info_buf;
-    sa.itemoff = ds->syrk_off;
+    sa.info = ds->info_buf + bt.info_at;
+    sa.itemoff = ds->syrk_off + bt.off_at;
     sa.Y = ds->y_buf;
     sa.scratch = ds->scratch;
-    syrk::compact_positions_kernel<<<dim3(n_i, 2, 2), 1024, 0, st>>>(d, sa, ds->pos_buf);
-    if (qmax > 0)
-      syrk::compact_gather_kernel<<<dim3((rmax + 127) / 128, qmax, n_i * 2), 128, 0, st>>>(
+    sa.debug_skip = ds->debug_skip;
+    sa.exact_count = ds->debug_counter;
+    syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, st>>>(d, sa, ds->pos_buf);
+    if (bt.qmax > 0)
+      syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0, st>>>(
           d, sa, ds->pos_buf, ds->y_buf);
-    const size_t tsm = tc::smem_bytes(K);
-    if (ranged) syrk::search_syrk_kernel<true><<<grid, tc::kThreads, tsm, st>>>(d, sa);
-    else syrk::search_syrk_kernel<false><<<grid, tc::kThreads, tsm, st>>>(d, sa);
+    if (ranged) syrk::search_syrk_kernel<true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    else syrk::search_syrk_kernel<false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     CUDA_TRY(cudaGetLastError());
     *launches += 3;
-    // infos/off are rewritten next batch; make sure the async copies consumed them
-    CUDA_TRY(cudaStreamSynchronize(st));
   }
+  // the host vectors die here: wait for their uploads only (kernels keep running)
+  CUDA_TRY(cudaEventSynchronize(ds->ev_upload));
   return E3_OK;
 }
 
@@ -931,8 +962,10 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   const uint32_t K = cfg->top_k;
   // Engines: compacted tensor-core SYRK (default), masked tensor-core GEMM,
   // LOP3/POPC. All produce identical results.
-  const uint32_t engine = cfg->flags & 3u;
-  const bool use_syrk = engine == 0;
+  uint32_t engine = cfg->flags & 3u;
+  if (engine == 0)  // auto: compaction pays off once the sample axis is long
+    engine = (ds->N[0] + ds->N[1]) >= 8192 ? E3_ENGINE_SYRK : E3_ENGINE_TC_MASKED;
+  const bool use_syrk = engine == E3_ENGINE_SYRK;
   const bool use_tc = engine == E3_ENGINE_TC_MASKED;
   uint32_t grid, nlists;
   tc::TcArgs ta{};

@@ -29,6 +29,7 @@ using namespace tc;
 constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows each
 constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
 constexpr int kScratchPerThread = kRounds * 16;  // u32: 8 values x 2 classes per round
+constexpr int kSyrkThreads = kThreads;  // warp 0 MMA, 1-8 producers, 9-16 epilogue
 
 // Per-i layout of the compacted operands (one record per i of the batch).
 struct IInfo {
@@ -52,6 +53,8 @@ struct SyrkArgs {
   const uint64_t* itemoff;           // [n_i + 1] tile prefix within the batch
   const uint4* Y;
   uint32_t* scratch;                 // [grid][kRounds * 16][256]
+  uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no K2, 2 = no expansion
+  unsigned long long* exact_count;   // profiling only: exact K2 evaluations (may be null)
 };
 
 // S_{i,a,c}: block-wide exclusive scan of popcounts over the class words of X_a^i.
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
             const uint32_t dcol = tmem + a * 256 + c * 128;
             for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
               const uint32_t st = n % kStages;
-              mbar_wait(&full_bar[st], (n / kStages) & 1);
+              mbar_wait_spin(&full_bar[st], (n / kStages) & 1);
               fence_after();
               const uint32_t abase = smem_u32(stages + st * kStageBytes);
               const uint32_t bbase = abase + kRows * kChunk;
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
     __syncwarp();
   } else if (warp <= kProducerWarps) {
     // ===================== producers: compacted bits -> bytes =====================
-    const int pt = threadIdx.x - 32;
+    const int pt = threadIdx.x - 32;            // 0..255
     const bool is_a = pt < kRows;
     const int r = is_a ? pt : pt - kRows;
     const uint32_t stage0 = smem_u32(stages) + (is_a ? 0 : kRows * kChunk);
@@ -266,28 +269,38 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
         for (uint32_t a = 0; a < 2; ++a) {
           const uint4* Ya = s.Y + inf.y_off[a] + rowi;
           const uint32_t qtot = inf.q[a][0] + inf.q[a][1];
-          // stages walk the quads of class 0 then class 1 (both even counts)
-          uint4 c0, c1;
-          if (qtot) {
-            c0 = __ldg(Ya);
-            c1 = __ldg(Ya + size_t(inf.R));
-          }
+          const uint32_t q0 = inf.q[a][0];
+          // stages walk the quads of class 0 then class 1 (both even counts);
+          // register prefetch of the next kAhead stages hides the L2 latency
+          constexpr uint32_t kAhead = 3;
+          uint4 pf[kAhead][2];
+#pragma unroll
+          for (uint32_t x = 0; x < kAhead; ++x)
+            if (2 * x < qtot) {
+              pf[x][0] = __ldg(Ya + size_t(2 * x) * inf.R);
+              pf[x][1] = __ldg(Ya + size_t(2 * x + 1) * inf.R);
+            }
           for (uint32_t q = 0; q < qtot; q += 2, ++n) {
-            uint4 n0 = c0, n1 = c1;
-            if (q + 2 < qtot) {
-              n0 = __ldg(Ya + size_t(q + 2) * inf.R);
-              n1 = __ldg(Ya + size_t(q + 3) * inf.R);
+            const uint4 c0 = pf[0][0], c1 = pf[0][1];
+#pragma unroll
+            for (uint32_t x = 0; x + 1 < kAhead; ++x) {
+              pf[x][0] = pf[x + 1][0];
+              pf[x][1] = pf[x + 1][1];
+            }
+            if (q + 2 * kAhead < qtot) {
+              pf[kAhead - 1][0] = __ldg(Ya + size_t(q + 2 * kAhead) * inf.R);
+              pf[kAhead - 1][1] = __ldg(Ya + size_t(q + 2 * kAhead + 1) * inf.R);
             }
             mbar_wait(&empty_bar[st], ph ^ 1);
             const uint32_t sb = stage0 + st * kStageBytes;
-            expand_quad(sb, r, 0, c0);
-            expand_quad(sb, r, 1, c1);
+            if (!(s.debug_skip & 2)) {
+              expand_quad(sb, r, 0, c0);
+              expand_quad(sb, r, 1, c1);
+            }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&full_bar[st]);
             if (++st == kStages) { st = 0; ph ^= 1; }
-            c0 = n0;
-            c1 = n1;
           }
         }
         wk.next(s);
@@ -404,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
             }
             const uint32_t k = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + tt;
             const uint32_t kc = min(k, M - 1);
-            bool valid = j < k && k < M;
+            bool valid = j < k && k < M && !(s.debug_skip & 1);
             if (kRanged && valid) {
               const uint64_t rr = rank_ij + (k - j - 1);
               valid = rr >= s.rank_begin && rr < s.rank_end;
@@ -418,6 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
               derive_cells(T1, pij1, __ldg(d.pair[1] + size_t(i) * M + kc),
                            __ldg(d.pair[1] + size_t(jc) * M + kc), si1, sj1,
                            __ldg(d.single[1] + kc), d.n[1], n1);
+              if (s.exact_count) atomicAdd(s.exact_count, 1ull);
               sk = score_key(k2_device(n0, n1, d.logp));
               tk = triple_key(i, j, k);
             }

@@ -95,9 +95,9 @@ class e3_plant(C.Structure):
 
 
 MAX_TOP_K = 256
-# e3_search_cfg.flags: 0 = compacted tensor-core SYRK (default),
-# E3_ENGINE_POPC = 1, E3_ENGINE_TC_MASKED = 2
-ENGINES = {"syrk": 0, "popc": 1, "tc_masked": 2}
+# e3_search_cfg.flags: 0 = auto, E3_ENGINE_POPC = 1, E3_ENGINE_TC_MASKED = 2,
+# E3_ENGINE_SYRK = 3
+ENGINES = {"auto": 0, "popc": 1, "tc_masked": 2, "syrk": 3}
 _P = C.c_void_p
 _U64 = C.c_uint64
 _U32 = C.c_uint32
@@ -331,7 +331,7 @@ class SearchConfig:
     top_k: int = 10
     rank_begin: int = 0
     rank_end: int = 0  # 0 = C(M,3)
-    engine: str = "syrk"  # "syrk" (default) | "tc_masked" | "popc" — identical results
+    engine: str = "auto"  # "auto" | "syrk" | "tc_masked" | "popc" — identical results
 
 
 def same_outcome(a: SearchResult, b: SearchResult) -> bool:
