@@ -582,36 +582,58 @@ struct e3_dataset {
 
 namespace {
 
+// Device memory comes from the device's stream-ordered pool with a release
+// threshold of "never", so dataset create/destroy cycles (the e2e path) reuse
+// cached blocks instead of paying cudaMalloc/cudaFree each time.
+template <typename T>
+cudaError_t dmalloc(const e3_dataset* ds, T** p, size_t bytes);
+template <typename T>
+void dfree(const e3_dataset* ds, T* p);
+
 void release(e3_dataset* ds) {
   if (!ds) return;
   cudaSetDevice(ds->device);
   for (int c = 0; c < 2; ++c) {
-    cudaFree(ds->planes[c]);
-    cudaFree(ds->single[c]);
-    cudaFree(ds->pair[c]);
-    cudaFree(ds->lists[c]);
-    cudaFree(ds->counts[c]);
+    dfree(ds, ds->planes[c]);
+    dfree(ds, ds->single[c]);
+    dfree(ds, ds->pair[c]);
+    dfree(ds, ds->lists[c]);
+    dfree(ds, ds->counts[c]);
   }
-  cudaFree(ds->logp);
-  cudaFree(ds->itemoff);
-  cudaFree(ds->itemoff_tc);
-  cudaFree(ds->y_buf);
-  cudaFree(ds->pos_buf);
-  cudaFree(ds->info_buf);
-  cudaFree(ds->syrk_off);
-  cudaFree(ds->scratch);
+  dfree(ds, ds->logp);
+  dfree(ds, ds->itemoff);
+  dfree(ds, ds->itemoff_tc);
+  dfree(ds, ds->y_buf);
+  dfree(ds, ds->pos_buf);
+  dfree(ds, ds->info_buf);
+  dfree(ds, ds->syrk_off);
+  dfree(ds, ds->scratch);
   if (ds->debug_counter) {
+    cudaStreamSynchronize(ds->stream);
     unsigned long long v = 0;
     cudaMemcpy(&v, ds->debug_counter, sizeof(v), cudaMemcpyDeviceToHost);
     std::fprintf(stderr, "[e3 debug] exact K2 evaluations: %llu\n", v);
-    cudaFree(ds->debug_counter);
+    dfree(ds, ds->debug_counter);
   }
-  cudaFree(ds->gthr);
+  dfree(ds, ds->gthr);
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
   if (ds->ev_upload) cudaEventDestroy(ds->ev_upload);
-  if (ds->stream) cudaStreamDestroy(ds->stream);
+  if (ds->stream) {
+    cudaStreamSynchronize(ds->stream);
+    cudaStreamDestroy(ds->stream);
+  }
   delete ds;
+}
+
+
+template <typename T>
+cudaError_t dmalloc(const e3_dataset* ds, T** p, size_t bytes) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, ds->stream);
+}
+template <typename T>
+void dfree(const e3_dataset* ds, T* p) {
+  if (p) cudaFreeAsync(const_cast<void*>(static_cast<const void*>(p)), ds->stream);
 }
 
 DevData dev_view(const e3_dataset* ds) {
@@ -631,6 +653,12 @@ DevData dev_view(const e3_dataset* ds) {
 
 int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaSetDevice(ds->device));
+  {
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, ds->device));
+    uint64_t keep = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
   for (auto& e : ds->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaEventCreateWithFlags(&ds->ev_upload, cudaEventDisableTiming));
@@ -639,17 +667,17 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   ds->num_sms = prop.multiProcessorCount;
   const uint32_t M = uint32_t(ds->M);
   uint32_t* bad = nullptr;
-  CUDA_TRY(cudaMalloc(&bad, sizeof(uint32_t)));
+  CUDA_TRY(dmalloc(ds, &bad, sizeof(uint32_t)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), ds->stream));
   for (int c = 0; c < 2; ++c) {
     const uint64_t n = ds->N[c];
     const uint32_t w64 = uint32_t((n + 63) / 64);
     ds->wq[c] = uint32_t((n + 127) / 128);
-    CUDA_TRY(cudaMalloc(&ds->single[c], sizeof(uint2) * M));
-    CUDA_TRY(cudaMalloc(&ds->pair[c], sizeof(uint4) * size_t(M) * M));
+    CUDA_TRY(dmalloc(ds, &ds->single[c], sizeof(uint2) * M));
+    CUDA_TRY(dmalloc(ds, &ds->pair[c], sizeof(uint4) * size_t(M) * M));
     // one extra zero quad: the search kernel steps two quads at a time
     const size_t plane_bytes = sizeof(uint4) * (size_t(ds->wq[c]) + 1) * M * 2;
-    CUDA_TRY(cudaMalloc(&ds->planes[c], plane_bytes));
+    CUDA_TRY(dmalloc(ds, &ds->planes[c], plane_bytes));
     CUDA_TRY(cudaMemsetAsync(ds->planes[c], 0, plane_bytes, ds->stream));
     if (ds->wq[c] == 0) {
       CUDA_TRY(cudaMemsetAsync(ds->single[c], 0, sizeof(uint2) * M, ds->stream));
@@ -658,7 +686,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     }
     uint64_t* raw = nullptr;
     const size_t raw_bytes = sizeof(uint64_t) * size_t(M) * 2 * w64;
-    CUDA_TRY(cudaMalloc(&raw, raw_bytes));
+    CUDA_TRY(dmalloc(ds, &raw, raw_bytes));
     CUDA_TRY(cudaMemcpyAsync(raw, host[c], raw_bytes, cudaMemcpyHostToDevice, ds->stream));
     const uint64_t rem = n % 64;
     const uint64_t tail = rem == 0 ? ~0ull : ((1ull << rem) - 1);
@@ -671,7 +699,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
                                                                  ds->pair[c]);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(ds->stream));
-    CUDA_TRY(cudaFree(raw));
+    dfree(ds, raw);
   }
   for (int c = 0; c < 2; ++c) {
     ds->h_single[c].resize(M);
@@ -682,7 +710,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   const uint64_t N = ds->N[0] + ds->N[1];
   std::vector<double> logp(N + 2);
   e3_build_log_table(N + 1, logp.data());
-  CUDA_TRY(cudaMalloc(&ds->logp, sizeof(double) * logp.size()));
+  CUDA_TRY(dmalloc(ds, &ds->logp, sizeof(double) * logp.size()));
   CUDA_TRY(cudaMemcpyAsync(ds->logp, logp.data(), sizeof(double) * logp.size(),
                            cudaMemcpyHostToDevice, ds->stream));
   // Item prefix over i (items = 32x32 (j,k) tiles above i, i-major).
@@ -691,14 +719,14 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     const uint64_t nt = (M - 1 - i + kTile - 1) / kTile;
     ds->h_itemoff[i + 1] = ds->h_itemoff[i] + nt * (nt + 1) / 2;
   }
-  CUDA_TRY(cudaMalloc(&ds->itemoff, sizeof(uint64_t) * ds->h_itemoff.size()));
+  CUDA_TRY(dmalloc(ds, &ds->itemoff, sizeof(uint64_t) * ds->h_itemoff.size()));
   CUDA_TRY(cudaMemcpyAsync(ds->itemoff, ds->h_itemoff.data(),
                            sizeof(uint64_t) * ds->h_itemoff.size(), cudaMemcpyHostToDevice,
                            ds->stream));
   ds->h_itemoff_tc.assign(M - 1, 0);
   for (uint32_t i = 0; i + 2 < M; ++i)
     ds->h_itemoff_tc[i + 1] = ds->h_itemoff_tc[i] + tc::items_of(M, i);
-  CUDA_TRY(cudaMalloc(&ds->itemoff_tc, sizeof(uint64_t) * ds->h_itemoff_tc.size()));
+  CUDA_TRY(dmalloc(ds, &ds->itemoff_tc, sizeof(uint64_t) * ds->h_itemoff_tc.size()));
   CUDA_TRY(cudaMemcpyAsync(ds->itemoff_tc, ds->h_itemoff_tc.data(),
                            sizeof(uint64_t) * ds->h_itemoff_tc.size(), cudaMemcpyHostToDevice,
                            ds->stream));
@@ -711,7 +739,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   ds->smem_optin = prop.sharedMemPerBlockOptin;
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   if (std::getenv("E3_DEBUG_COUNT")) {
-    CUDA_TRY(cudaMalloc(&ds->debug_counter, sizeof(unsigned long long)));
+    CUDA_TRY(dmalloc(ds, &ds->debug_counter, sizeof(unsigned long long)));
     CUDA_TRY(cudaMemset(ds->debug_counter, 0, sizeof(unsigned long long)));
   }
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false>,
@@ -720,11 +748,11 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaMalloc(&ds->gthr, sizeof(uint64_t)));
+  CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
   uint32_t h_bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
   CUDA_TRY(cudaStreamSynchronize(ds->stream));
-  CUDA_TRY(cudaFree(bad));
+  dfree(ds, bad);
   if (h_bad)
     return fail(E3_DOMAIN,
                 "bit planes violate the dataset invariants (overlapping genotype planes or "
@@ -863,25 +891,25 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   // batch b+1's compaction can overlap nothing it must not touch (same stream:
   // ordering is by the stream; two buffers keep the option of a second stream)
   if (ymax > ds->y_cap) {
-    cudaFree(ds->y_buf);
+    dfree(ds, ds->y_buf);
     ds->y_buf = nullptr;
-    CUDA_TRY(cudaMalloc(&ds->y_buf, sizeof(uint4) * std::max<size_t>(ymax, 1)));
+    CUDA_TRY(dmalloc(ds, &ds->y_buf, sizeof(uint4) * std::max<size_t>(ymax, 1)));
     ds->y_cap = ymax;
   }
   if (pmax > ds->pos_cap) {
-    cudaFree(ds->pos_buf);
+    dfree(ds, ds->pos_buf);
     ds->pos_buf = nullptr;
-    CUDA_TRY(cudaMalloc(&ds->pos_buf, sizeof(uint32_t) * std::max<size_t>(pmax, 1)));
+    CUDA_TRY(dmalloc(ds, &ds->pos_buf, sizeof(uint32_t) * std::max<size_t>(pmax, 1)));
     ds->pos_cap = pmax;
   }
   const size_t info_need = infos.size() + offs.size();
   if (info_need > ds->info_cap) {
-    cudaFree(ds->info_buf);
-    cudaFree(ds->syrk_off);
+    dfree(ds, ds->info_buf);
+    dfree(ds, ds->syrk_off);
     ds->info_buf = nullptr;
     ds->syrk_off = nullptr;
-    CUDA_TRY(cudaMalloc(&ds->info_buf, sizeof(syrk::IInfo) * std::max<size_t>(infos.size(), 1)));
-    CUDA_TRY(cudaMalloc(&ds->syrk_off, sizeof(uint64_t) * std::max<size_t>(offs.size(), 1)));
+    CUDA_TRY(dmalloc(ds, &ds->info_buf, sizeof(syrk::IInfo) * std::max<size_t>(infos.size(), 1)));
+    CUDA_TRY(dmalloc(ds, &ds->syrk_off, sizeof(uint64_t) * std::max<size_t>(offs.size(), 1)));
     ds->info_cap = info_need;
   }
   CUDA_TRY(cudaMemcpyAsync(ds->info_buf, infos.data(), sizeof(syrk::IInfo) * infos.size(),
@@ -890,7 +918,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
                            cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(ds->ev_upload, st));
   if (!ds->scratch)
-    CUDA_TRY(cudaMalloc(&ds->scratch, sizeof(uint32_t) * size_t(grid) *
+    CUDA_TRY(dmalloc(ds, &ds->scratch, sizeof(uint32_t) * size_t(grid) *
                                           syrk::kScratchPerThread * 256));
   CUDA_TRY(cudaMemsetAsync(ds->counts[0], 0, sizeof(uint32_t) * grid * tc::kEpilogueWarps, st));
   const size_t tsm = tc::smem_bytes(K);
@@ -986,12 +1014,12 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   const size_t need = size_t(nlists) * K;
   if (need > ds->lists_cap || nlists > ds->counts_cap) {
     for (int b = 0; b < 2; ++b) {
-      cudaFree(ds->lists[b]);
-      cudaFree(ds->counts[b]);
+      dfree(ds, ds->lists[b]);
+      dfree(ds, ds->counts[b]);
       ds->lists[b] = nullptr;
       ds->counts[b] = nullptr;
-      CUDA_TRY(cudaMalloc(&ds->lists[b], sizeof(ulonglong2) * need));
-      CUDA_TRY(cudaMalloc(&ds->counts[b], sizeof(uint32_t) * nlists));
+      CUDA_TRY(dmalloc(ds, &ds->lists[b], sizeof(ulonglong2) * need));
+      CUDA_TRY(dmalloc(ds, &ds->counts[b], sizeof(uint32_t) * nlists));
     }
     ds->lists_cap = need;
     ds->counts_cap = nlists;
@@ -1097,9 +1125,9 @@ int run_triples(const e3_dataset* ds, const uint32_t* triples, uint64_t n, uint3
   uint32_t* d_tri = nullptr;
   uint32_t* d_tab = nullptr;
   double* d_sc = nullptr;
-  CUDA_TRY(cudaMalloc(&d_tri, sizeof(uint32_t) * 3 * n));
-  if (tables) CUDA_TRY(cudaMalloc(&d_tab, sizeof(uint32_t) * 54 * n));
-  if (scores) CUDA_TRY(cudaMalloc(&d_sc, sizeof(double) * n));
+  CUDA_TRY(dmalloc(ds, &d_tri, sizeof(uint32_t) * 3 * n));
+  if (tables) CUDA_TRY(dmalloc(ds, &d_tab, sizeof(uint32_t) * 54 * n));
+  if (scores) CUDA_TRY(dmalloc(ds, &d_sc, sizeof(double) * n));
   cudaStream_t st = ds->stream;
   CUDA_TRY(cudaMemcpyAsync(d_tri, triples, sizeof(uint32_t) * 3 * n, cudaMemcpyHostToDevice, st));
   triples_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(dev_view(ds), d_tri, n, d_tab, d_sc);
@@ -1109,9 +1137,9 @@ int run_triples(const e3_dataset* ds, const uint32_t* triples, uint64_t n, uint3
   if (scores)
     CUDA_TRY(cudaMemcpyAsync(scores, d_sc, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  cudaFree(d_tri);
-  cudaFree(d_tab);
-  cudaFree(d_sc);
+  dfree(ds, d_tri);
+  dfree(ds, d_tab);
+  dfree(ds, d_sc);
   return E3_OK;
 }
 }  // namespace
