@@ -569,7 +569,6 @@ struct e3_dataset {
   int num_sms = 0, search_ctas_per_sm = 0, search_min_blocks = 1;
   size_t smem_optin = 0;
   uint32_t debug_skip = 0;  // E3_DEBUG_SKIP (profiling experiments only)
-  unsigned long long* debug_counter = nullptr;  // E3_DEBUG_COUNT: exact-K2 evaluations
   // scratch reused across searches
   ulonglong2* lists[2] = {nullptr, nullptr};
   uint32_t* counts[2] = {nullptr, nullptr};
@@ -608,13 +607,6 @@ void release(e3_dataset* ds) {
   dfree(ds, ds->info_buf);
   dfree(ds, ds->syrk_off);
   dfree(ds, ds->scratch);
-  if (ds->debug_counter) {
-    cudaStreamSynchronize(ds->stream);
-    unsigned long long v = 0;
-    cudaMemcpy(&v, ds->debug_counter, sizeof(v), cudaMemcpyDeviceToHost);
-    std::fprintf(stderr, "[e3 debug] exact K2 evaluations: %llu\n", v);
-    dfree(ds, ds->debug_counter);
-  }
   dfree(ds, ds->gthr);
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
@@ -738,10 +730,6 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
                                 int(tc::smem_bytes(E3_MAX_TOP_K))));
   ds->smem_optin = prop.sharedMemPerBlockOptin;
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
-  if (std::getenv("E3_DEBUG_COUNT")) {
-    CUDA_TRY(dmalloc(ds, &ds->debug_counter, sizeof(unsigned long long)));
-    CUDA_TRY(cudaMemset(ds->debug_counter, 0, sizeof(unsigned long long)));
-  }
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
@@ -939,7 +927,6 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.Y = ds->y_buf;
     sa.scratch = ds->scratch;
     sa.debug_skip = ds->debug_skip;
-    sa.exact_count = ds->debug_counter;
     syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, st>>>(d, sa, ds->pos_buf);
     if (bt.qmax > 0)
       syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0, st>>>(

@@ -29,7 +29,11 @@ using namespace tc;
 constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows each
 constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
 constexpr int kScratchPerThread = kRounds * 16;  // u32: 8 values x 2 classes per round
-constexpr int kSyrkThreads = kThreads;  // warp 0 MMA, 1-8 producers, 9-16 epilogue
+// 13 warps: warp 0 issues the MMAs, warps 1-4 expand operands (each thread one
+// A row and one B row), warps 5-12 run the epilogue. With 13 warps no SM
+// sub-partition holds more than 4, so each thread may use 128 registers.
+constexpr int kSyrkProducerWarps = 4;
+constexpr int kSyrkThreads = 32 * (1 + kSyrkProducerWarps + kEpilogueWarps);
 
 // Per-i layout of the compacted operands (one record per i of the batch).
 struct IInfo {
@@ -54,7 +58,6 @@ struct SyrkArgs {
   const uint4* Y;
   uint32_t* scratch;                 // [grid][kRounds * 16][256]
   uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no K2, 2 = no expansion
-  unsigned long long* exact_count;   // profiling only: exact K2 evaluations (may be null)
 };
 
 // S_{i,a,c}: block-wide exclusive scan of popcounts over the class words of X_a^i.
@@ -178,7 +181,7 @@ struct SWalker {
 };
 
 template <bool kRanged>
-__global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
+__global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
-      mbar_init(&full_bar[st], kProducerWarps);
+      mbar_init(&full_bar[st], kSyrkProducerWarps);
       mbar_init(&empty_bar[st], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -251,51 +254,56 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
       }
     }
     __syncwarp();
-  } else if (warp <= kProducerWarps) {
+  } else if (warp <= kSyrkProducerWarps) {
     // ===================== producers: compacted bits -> bytes =====================
-    const int pt = threadIdx.x - 32;            // 0..255
-    const bool is_a = pt < kRows;
-    const int r = is_a ? pt : pt - kRows;
-    const uint32_t stage0 = smem_u32(stages) + (is_a ? 0 : kRows * kChunk);
+    // Each thread owns A row r and B row r; the Y words of the next kAhead
+    // stages are prefetched into registers (L2 latency hidden).
+    const int r = threadIdx.x - 32;             // 0..127
+    const uint32_t stage_a = smem_u32(stages), stage_b = stage_a + kRows * kChunk;
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
-      uint32_t n = 0;
       uint32_t st = 0, ph = 0;
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo inf = s.info[wk.ii];
-        const uint32_t rowi = min((is_a ? wk.jb : wk.kb) * 2 * kJB + r, inf.R - 1);
+        const uint32_t row_a = min(wk.jb * 2 * kJB + r, inf.R - 1);
+        const uint32_t row_b = min(wk.kb * 2 * kJB + r, inf.R - 1);
 #pragma unroll
         for (uint32_t a = 0; a < 2; ++a) {
-          const uint4* Ya = s.Y + inf.y_off[a] + rowi;
+          const uint4* Ya = s.Y + inf.y_off[a] + row_a;
+          const uint4* Yb = s.Y + inf.y_off[a] + row_b;
+          const size_t R = inf.R;
           const uint32_t qtot = inf.q[a][0] + inf.q[a][1];
-          const uint32_t q0 = inf.q[a][0];
-          // stages walk the quads of class 0 then class 1 (both even counts);
-          // register prefetch of the next kAhead stages hides the L2 latency
-          constexpr uint32_t kAhead = 3;
-          uint4 pf[kAhead][2];
+          constexpr uint32_t kAhead = 2;
+          uint4 pa[kAhead][2], pb[kAhead][2];
 #pragma unroll
           for (uint32_t x = 0; x < kAhead; ++x)
             if (2 * x < qtot) {
-              pf[x][0] = __ldg(Ya + size_t(2 * x) * inf.R);
-              pf[x][1] = __ldg(Ya + size_t(2 * x + 1) * inf.R);
+              pa[x][0] = __ldg(Ya + (2 * x) * R);
+              pa[x][1] = __ldg(Ya + (2 * x + 1) * R);
+              pb[x][0] = __ldg(Yb + (2 * x) * R);
+              pb[x][1] = __ldg(Yb + (2 * x + 1) * R);
             }
-          for (uint32_t q = 0; q < qtot; q += 2, ++n) {
-            const uint4 c0 = pf[0][0], c1 = pf[0][1];
+          for (uint32_t q = 0; q < qtot; q += 2) {
+            const uint4 a0 = pa[0][0], a1 = pa[0][1], b0 = pb[0][0], b1 = pb[0][1];
 #pragma unroll
             for (uint32_t x = 0; x + 1 < kAhead; ++x) {
-              pf[x][0] = pf[x + 1][0];
-              pf[x][1] = pf[x + 1][1];
+              pa[x][0] = pa[x + 1][0]; pa[x][1] = pa[x + 1][1];
+              pb[x][0] = pb[x + 1][0]; pb[x][1] = pb[x + 1][1];
             }
             if (q + 2 * kAhead < qtot) {
-              pf[kAhead - 1][0] = __ldg(Ya + size_t(q + 2 * kAhead) * inf.R);
-              pf[kAhead - 1][1] = __ldg(Ya + size_t(q + 2 * kAhead + 1) * inf.R);
+              const size_t o = size_t(q + 2 * kAhead) * R;
+              pa[kAhead - 1][0] = __ldg(Ya + o);
+              pa[kAhead - 1][1] = __ldg(Ya + o + R);
+              pb[kAhead - 1][0] = __ldg(Yb + o);
+              pb[kAhead - 1][1] = __ldg(Yb + o + R);
             }
             mbar_wait(&empty_bar[st], ph ^ 1);
-            const uint32_t sb = stage0 + st * kStageBytes;
             if (!(s.debug_skip & 2)) {
-              expand_quad(sb, r, 0, c0);
-              expand_quad(sb, r, 1, c1);
+              expand_quad(stage_a + st * kStageBytes, r, 0, a0);
+              expand_quad(stage_a + st * kStageBytes, r, 1, a1);
+              expand_quad(stage_b + st * kStageBytes, r, 0, b0);
+              expand_quad(stage_b + st * kStageBytes, r, 1, b1);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
@@ -305,11 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
         }
         wk.next(s);
       }
-      (void)n;
     }
   } else {
     // ===================== epilogue =====================
-    const int ew = warp - 1 - kProducerWarps;   // 0..7
+    const int ew = warp - 1 - kSyrkProducerWarps;  // 0..7
     const int half = ew >> 2;                   // k columns [32*half, 32*half+32)
     const int quarter = warp & 3;               // TMEM lane quarter
     const int et = ew * 32 + lane;              // 0..255 scratch slot
@@ -431,7 +438,6 @@ __global__ void __launch_bounds__(kThreads, 1) search_syrk_kernel(const DevData 
               derive_cells(T1, pij1, __ldg(d.pair[1] + size_t(i) * M + kc),
                            __ldg(d.pair[1] + size_t(jc) * M + kc), si1, sj1,
                            __ldg(d.single[1] + kc), d.n[1], n1);
-              if (s.exact_count) atomicAdd(s.exact_count, 1ull);
               sk = score_key(k2_device(n0, n1, d.logp));
               tk = triple_key(i, j, k);
             }
