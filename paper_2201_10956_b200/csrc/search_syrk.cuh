@@ -28,7 +28,7 @@ using namespace tc;
 
 constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows each
 constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
-constexpr int kScratchPerThread = kRounds * 16;  // u32: 8 values x 2 classes per round
+constexpr int kScratchPerThread = kRounds * 32;  // u32: 8 values x 2 classes x 2 phases per round
 // 13 warps: warp 0 issues the MMAs, warps 1-4 expand operands (each thread one
 // A row and one B row), warps 5-12 run the epilogue. With 13 warps no SM
 // sub-partition holds more than 4, so each thread may use 128 registers.
@@ -357,9 +357,25 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         }
         fence_before();
         mbar_arrive(&tempty_bar[0]);
-        // ---- phase a = 1: TMEM + scratch -> cells -> K2 -> top-k
+        // ---- phase a = 1: TMEM -> scratch, then release TMEM before scoring, so
+        // the K2 work of this tile overlaps the next tile's MMAs.
         mbar_wait_sleep(&tfull_bar[1], t2 & 1);
         fence_after();
+        for (int m = 0; m < kRounds; ++m) {
+          uint32_t v0[8], v1[8];
+          const uint32_t taddr =
+              tmem + (uint32_t(quarter * 32) << 16) + 256 + 8 * (half * kRounds + m);
+          tmem_ld8(taddr, v0);
+          tmem_ld8(taddr + 128, v1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            scr[(kRounds * 16 + m * 16 + x) * 256] = inf.q[1][0] ? v0[x] : 0u;
+            scr[(kRounds * 16 + m * 16 + 8 + x) * 256] = inf.q[1][1] ? v1[x] : 0u;
+          }
+        }
+        fence_before();
+        mbar_arrive(&tempty_bar[1]);
         const uint32_t j = i + 1 + wk.jb * kJB + jl;
         const uint32_t jc = min(j, M - 1);
         const uint64_t gth = *reinterpret_cast<volatile uint64_t*>(s.gthr);
@@ -375,18 +391,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
         for (int m = 0; m < kRounds; ++m) {
           uint32_t v0[8], v1[8], u0[8], u1[8];
-          const uint32_t taddr =
-              tmem + (uint32_t(quarter * 32) << 16) + 256 + 8 * (half * kRounds + m);
-          tmem_ld8(taddr, v0);
-          tmem_ld8(taddr + 128, v1);
 #pragma unroll
           for (int x = 0; x < 8; ++x) {
             u0[x] = scr[(m * 16 + x) * 256];
             u1[x] = scr[(m * 16 + 8 + x) * 256];
+            v0[x] = scr[(kRounds * 16 + m * 16 + x) * 256];
+            v1[x] = scr[(kRounds * 16 + m * 16 + 8 + x) * 256];
           }
-          tmem_wait_ld();
-          if (inf.q[1][0] == 0) for (int x = 0; x < 8; ++x) v0[x] = 0;
-          if (inf.q[1][1] == 0) for (int x = 0; x < 8; ++x) v1[x] = 0;
           // This thread holds T_a[b=bsel][g] for k phases t=0..3 (index 2t+g),
           // a=0 in u (scratch), a=1 in v (TMEM). Thread b owns phases 2b, 2b+1;
           // it sends the partner (b^1) its values for the partner's phases.
@@ -447,8 +458,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             if (cand) warp_insert(ls, lt, nlist, K, cand, sk, tk, lane, s.gthr);
           }
         }
-        fence_before();
-        mbar_arrive(&tempty_bar[1]);
         wk.next(s);
       }
     }
