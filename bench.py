@@ -171,9 +171,17 @@ def main():
     import torch.distributed as dist
     from paper_2201_10956_b200 import epi3
 
+    # E3_BENCH_BACKEND=gloo lets the multi-rank path be exercised with ranks
+    # sharing one GPU (testing only; NCCL needs one GPU per rank)
+    backend = os.environ.get("E3_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
         if world > 1:
@@ -259,12 +267,14 @@ def main():
 
     # ---- reduce over ranks (max time) --------------------------------------
     t = torch.tensor([dev_ms, kern_ms, e2e["secs"] if e2e else 0.0], dtype=torch.float64,
-                     device="cuda")
+                     device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         # the one collective of the search: all-gather + merge of the top-k
         from paper_2201_10956_b200 import partition
         merged = partition.allgather_merge(results[-1], top_k)
+    else:
+        merged = results[-1]
     dev_ms, kern_ms, e2e_secs = t.tolist()
     tot_elements = elements * world
 
@@ -338,6 +348,8 @@ def main():
                              engine=args.engine, kernel_ms_per_step=kern_ms / args.steps,
                              traffic=traffic),
             "cpu_baseline": cpu,
+            "last_step_best": {"triple": list(merged.best.triple), "k2": merged.best.score,
+                               "merged_over_ranks": world},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
