@@ -97,6 +97,9 @@ struct DevData {
   const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y)
   const double* logp;        // build_log_table(N+1): N+2 entries
   const uint64_t* itemoff;   // [M-1] prefix item counts per i
+  const float* ktab;         // screening table G[n] = fl32(logp[n] - alpha*n), ktab_n entries
+  uint32_t ktab_n;           // N+2 rounded up to a multiple of 4
+  double kshift;             // -27*alpha + proven screening error bound
 };
 
 // ------------------------------------------------------------------------
@@ -157,6 +160,22 @@ __device__ __forceinline__ double k2_device(const uint32_t* n0, const uint32_t* 
   return score;
 }
 
+
+// fp32 screen of k2_score: sum_c (G[r0+r1+1] - G[r0]) - G[r1] over a
+// shared-memory table G[n] = fl32(P[n] - alpha*n). The affine shift cancels
+// per cell up to the constant alpha, so score = screen + 27*alpha up to an
+// error the host bounds rigorously (k2_screen_margin); only triples whose
+// screen passes the current threshold are scored exactly with k2_device.
+__device__ __forceinline__ float k2_screen(const uint32_t* n0, const uint32_t* n1,
+                                           const float* G) {
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < 27; ++c) {
+    const uint32_t r0 = n0[c], r1 = n1[c];
+    s = __fadd_rn(s, __fsub_rn(__fsub_rn(G[r0 + r1 + 1], G[r0]), G[r1]));
+  }
+  return s;
+}
 
 // One 32-sample word of one class for one (i, j, k): 8 AND3 + 8 POPC.
 __device__ __forceinline__ void count_word(uint32_t xi0, uint32_t xi1, uint32_t xj0, uint32_t xj1,
@@ -552,6 +571,9 @@ struct e3_dataset {
   uint2* single[2] = {nullptr, nullptr};
   uint4* pair[2] = {nullptr, nullptr};
   double* logp = nullptr;
+  float* ktab = nullptr;              // K2 screening table (see k2_screen)
+  uint32_t ktab_n = 0;
+  double kshift = 0;
   uint64_t* itemoff = nullptr;
   std::vector<uint64_t> h_itemoff;
   uint64_t* itemoff_tc = nullptr;     // tensor-core kernel item prefix (32-j x 64-k tiles)
@@ -600,6 +622,7 @@ void release(e3_dataset* ds) {
     dfree(ds, ds->counts[c]);
   }
   dfree(ds, ds->logp);
+  dfree(ds, ds->ktab);
   dfree(ds, ds->itemoff);
   dfree(ds, ds->itemoff_tc);
   dfree(ds, ds->y_buf);
@@ -640,7 +663,25 @@ DevData dev_view(const e3_dataset* ds) {
   }
   d.logp = ds->logp;
   d.itemoff = ds->itemoff;
+  d.ktab = ds->ktab;
+  d.ktab_n = ds->ktab_n;
+  d.kshift = ds->kshift;
   return d;
+}
+
+// Rigorous bound on |screen + 27*alpha - score| for k2_screen with table
+// entries |G[n]| <= gmax, in round-to-nearest fp32 (unit roundoff u = 2^-24):
+// per cell three table roundings (<= u*gmax each), two subtractions
+// (|result| <= 2*gmax, 3*gmax) and one accumulation into a partial sum
+// bounded by smax. smax: a score is sum_c log((n_c+1)! / (r0! r1!)) =
+// sum_c log((n_c+1) C(n_c, r0)) <= N ln 2 + 27 ln(N+1), each term >= 0, and
+// the shifted terms subtract alpha. Doubled, plus slack for the fp64
+// rounding of the reference score itself.
+double k2_screen_margin(double gmax, double N, double alpha) {
+  const double u = std::ldexp(1.0, -24);
+  const double smax = N * std::log(2.0) + 27.0 * std::log(N + 1.0) + 27.0 * std::fabs(alpha) + 1.0;
+  const double per_cell = u * (3.0 * gmax + 2.0 * gmax + 3.0 * gmax + smax) * (1.0 + 4.0 * u);
+  return 2.0 * 27.0 * per_cell + 1e-9 * smax + 1e-6;
 }
 
 int build(e3_dataset* ds, const uint64_t* host[2]) {
@@ -704,6 +745,22 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   e3_build_log_table(N + 1, logp.data());
   CUDA_TRY(dmalloc(ds, &ds->logp, sizeof(double) * logp.size()));
   CUDA_TRY(cudaMemcpyAsync(ds->logp, logp.data(), sizeof(double) * logp.size(),
+                           cudaMemcpyHostToDevice, ds->stream));
+  // K2 screening table G[n] = fl32(P[n] - alpha*n): alpha balances the extremes
+  // of P[n] - alpha*n over [0, N+1] (about -0.28 N .. +0.28 N), which keeps the
+  // fp32 rounding small; the affine part cancels per cell up to alpha.
+  const double alpha = std::log(double(N) + 1.0) - 1.2785;
+  ds->ktab_n = uint32_t((N + 2 + 3) / 4 * 4);
+  std::vector<float> ktab(ds->ktab_n, 0.f);
+  double gmax = 0;
+  for (uint64_t n = 0; n < N + 2; ++n) {
+    const double g = logp[n] - alpha * double(n);
+    ktab[n] = float(g);
+    gmax = std::max(gmax, std::fabs(g));
+  }
+  ds->kshift = -27.0 * alpha + k2_screen_margin(gmax, double(N), alpha);
+  CUDA_TRY(dmalloc(ds, &ds->ktab, sizeof(float) * ktab.size()));
+  CUDA_TRY(cudaMemcpyAsync(ds->ktab, ktab.data(), sizeof(float) * ktab.size(),
                            cudaMemcpyHostToDevice, ds->stream));
   // Item prefix over i (items = 32x32 (j,k) tiles above i, i-major).
   ds->h_itemoff.assign(M - 1, 0);
@@ -909,7 +966,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     CUDA_TRY(dmalloc(ds, &ds->scratch, sizeof(uint32_t) * size_t(grid) *
                                           syrk::kScratchPerThread * 256));
   CUDA_TRY(cudaMemsetAsync(ds->counts[0], 0, sizeof(uint32_t) * grid * tc::kEpilogueWarps, st));
-  const size_t tsm = tc::smem_bytes(K);
+  size_t tsm = 1024 + size_t(syrk::kSStages) * syrk::kSStageBytes +
+               size_t(tc::kEpilogueWarps) * 2 * K * sizeof(uint64_t);
+  // the K2 screen needs its table in shared memory; without room, every
+  // valid triple is scored exactly from the global fp64 table
+  const bool screen = tsm + sizeof(float) * ds->ktab_n <= ds->smem_optin - 2048 &&
+                      !std::getenv("E3_NO_SCREEN");
+  if (screen) tsm += sizeof(float) * ds->ktab_n;
   for (const Batch& bt : batches) {
     syrk::SyrkArgs sa{};
     sa.item_begin = 0;
@@ -927,6 +990,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.Y = ds->y_buf;
     sa.scratch = ds->scratch;
     sa.debug_skip = ds->debug_skip;
+    sa.screen = screen ? 1u : 0u;
     syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, st>>>(d, sa, ds->pos_buf);
     if (bt.qmax > 0)
       syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0, st>>>(
@@ -978,8 +1042,12 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   // Engines: compacted tensor-core SYRK (default), masked tensor-core GEMM,
   // LOP3/POPC. All produce identical results.
   uint32_t engine = cfg->flags & 3u;
+  // the SYRK engine accumulates exact counts in f32 (fp4 operands): N_c < 2^23
+  const bool syrk_ok = std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 23);
   if (engine == 0)  // auto: compaction pays off once the sample axis is long
-    engine = (ds->N[0] + ds->N[1]) >= 8192 ? E3_ENGINE_SYRK : E3_ENGINE_TC_MASKED;
+    engine = (ds->N[0] + ds->N[1]) >= 8192 && syrk_ok ? E3_ENGINE_SYRK : E3_ENGINE_TC_MASKED;
+  if (engine == E3_ENGINE_SYRK && !syrk_ok)
+    return fail(E3_DOMAIN, "the SYRK engine supports at most 2^23 - 1 samples per class");
   const bool use_syrk = engine == E3_ENGINE_SYRK;
   const bool use_tc = engine == E3_ENGINE_TC_MASKED;
   uint32_t grid, nlists;

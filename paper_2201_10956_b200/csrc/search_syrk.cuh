@@ -27,6 +27,59 @@ namespace syrk {
 using namespace tc;
 
 constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows each
+// Operands are packed E2M1 (fp4, two samples per byte; 1.0 = nibble 0x2),
+// multiplied by tcgen05.mma kind::mxf4 with all block scales = 1.0 and f32
+// accumulation, which is exact for counts < 2^24 (host requires N_c < 2^23).
+constexpr int kSChunk = 256;                           // samples per stage
+constexpr int kSRowBytes = kSChunk / 2;                // 128 B per operand row
+constexpr int kSStageBytes = 2 * kRows * kSRowBytes;   // A + B = 32 KiB
+constexpr int kSStages = 4;
+constexpr int kUnits = 3;          // TMEM ring of (tile, a, c) accumulators, 128 columns each
+constexpr uint32_t kSfCol = 384;   // scale-factor columns (UE8M0 1.0)
+constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10)          // A, B = E2M1
+                            | (uint32_t(128 >> 3) << 17)      // N = 128
+                            | (1u << 23)                      // scale type UE8M0
+                            | (uint32_t(128 >> 4) << 24);     // M = 128, K = 64
+
+// K-major no-swizzle descriptor for a 128-byte stage row (8 16-byte slabs).
+__device__ __forceinline__ uint64_t f4_desc(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3fff) | (uint64_t(128 >> 4) << 16) |
+         (uint64_t((kSRowBytes / 16) * 128 >> 4) << 32) | (uint64_t(1) << 46);
+}
+__device__ __forceinline__ void mma_f4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t tsf, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdescF4), "r"(accumulate), "r"(tsf));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+// Exact f32 count (< 2^23) -> u32: adding 2^23 puts the integer in the mantissa.
+__device__ __forceinline__ uint32_t f32_count(uint32_t bits) {
+  return __float_as_uint(__uint_as_float(bits) + 8388608.f) - 0x4B000000u;
+}
+// One 128-sample quad -> slabs [4h, 4h+4) (16 B = 32 samples each) of an
+// operand row. Slab word t holds, in nibble n, sample 4n+t of the quad word
+// as E2M1 1.0 (0x2) or 0: a fixed permutation of the sample axis, identical
+// for A and B, so every dot product is unchanged.
+__device__ __forceinline__ void expand_quad_f4(uint32_t row_saddr, int h, uint4 q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint32_t v = w[x];
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row_saddr + (4 * h + x) * 128),
+                 "r"((v << 1) & 0x22222222u), "r"(v & 0x22222222u), "r"((v >> 1) & 0x22222222u),
+                 "r"((v >> 2) & 0x22222222u)
+                 : "memory");
+  }
+}
 constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
 constexpr int kScratchPerThread = kRounds * 32;  // u32: 8 values x 2 classes x 2 phases per round
 // 13 warps: warp 0 issues the MMAs, warps 1-4 expand operands (each thread one
@@ -58,6 +111,7 @@ struct SyrkArgs {
   const uint4* Y;
   uint32_t* scratch;                 // [grid][kRounds * 16][256]
   uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no K2, 2 = no expansion
+  uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
 };
 
 // S_{i,a,c}: block-wide exclusive scan of popcounts over the class words of X_a^i.
@@ -186,9 +240,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* stages = smem;
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
-  __shared__ uint64_t tfull_bar[2], tempty_bar[2];
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + kSStages * kSStageBytes);
+  float* ktab = reinterpret_cast<float*>(lists + size_t(kEpilogueWarps) * 2 * s.top_k);
+  __shared__ uint64_t full_bar[kSStages], empty_bar[kSStages];
+  __shared__ uint64_t tfull_bar[kUnits], tempty_bar[kUnits];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -198,11 +253,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   const uint64_t it1 = s.item_begin + s.item_count * (blockIdx.x + 1) / gridDim.x;
 
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kStages; ++st) {
+    for (int st = 0; st < kSStages; ++st) {
       mbar_init(&full_bar[st], kSyrkProducerWarps);
       mbar_init(&empty_bar[st], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kUnits; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 32 * kEpilogueWarps);
     }
@@ -213,53 +268,76 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                      smem_u32(&tmem_base_sh)), "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if (s.screen) {  // K2 screening table -> shared memory
+    const float4* src = reinterpret_cast<const float4*>(d.ktab);
+    float4* dst = reinterpret_cast<float4*>(ktab);
+    for (uint32_t x = threadIdx.x; x < d.ktab_n / 4; x += blockDim.x) dst[x] = __ldg(src + x);
+  }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base_sh;
+  // Block scale factors = 1.0 (UE8M0 0x7F) in columns [kSfCol, kSfCol+32) of
+  // all 128 lanes: one epilogue warp per TMEM lane quarter writes them.
+  if (warp > kSyrkProducerWarps && warp <= kSyrkProducerWarps + 4) {
+    const uint32_t addr = tmem + (uint32_t((warp & 3) * 32) << 16) + kSfCol;
+    const uint32_t one = 0x7F7F7F7Fu;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
+        "r"(one)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
 
   if (warp == 0) {
     // ===================== MMA issuer (one thread) =====================
+    // Units (tile, a, c) in order; unit u accumulates into ring slot u % kUnits.
     if (lane == 0 && it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
-      uint32_t n = 0;
+      uint32_t n = 0, u = 0;
+      const uint32_t tsf = tmem + kSfCol;
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo& inf = s.info[wk.ii];
 #pragma unroll
         for (uint32_t a = 0; a < 2; ++a) {
-          const uint32_t t2 = uint32_t(it - it0);  // phase a of tile t uses buffer a
-          mbar_wait(&tempty_bar[a], (t2 & 1) ^ 1);
-          fence_after();
 #pragma unroll
-          for (uint32_t c = 0; c < 2; ++c) {
+          for (uint32_t c = 0; c < 2; ++c, ++u) {
+            const uint32_t slot = u % kUnits;
+            mbar_wait(&tempty_bar[slot], ((u / kUnits) & 1) ^ 1);
+            fence_after();
             const uint32_t nch = inf.q[a][c] / 2;
-            const uint32_t dcol = tmem + a * 256 + c * 128;
+            const uint32_t dcol = tmem + slot * 128;
             for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
-              const uint32_t st = n % kStages;
-              mbar_wait_spin(&full_bar[st], (n / kStages) & 1);
+              const uint32_t st = n % kSStages;
+              mbar_wait_spin(&full_bar[st], (n / kSStages) & 1);
               fence_after();
-              const uint32_t abase = smem_u32(stages + st * kStageBytes);
-              const uint32_t bbase = abase + kRows * kChunk;
+              const uint32_t abase = smem_u32(stages + st * kSStageBytes);
+              const uint32_t bbase = abase + kRows * kSRowBytes;
 #pragma unroll
-              for (int kk = 0; kk < kChunk / 32; ++kk)
-                mma_i8(dcol, smem_desc(abase + kk * 256), smem_desc(bbase + kk * 256),
+              for (int kk = 0; kk < kSRowBytes / 32; ++kk)
+                mma_f4(dcol, f4_desc(abase + kk * 256), f4_desc(bbase + kk * 256), tsf,
                        (ch != 0 || kk != 0) ? 1u : 0u);
               mma_commit(&empty_bar[st]);
             }
+            mma_commit(&tfull_bar[slot]);
           }
-          mma_commit(&tfull_bar[a]);
         }
         wk.next(s);
       }
     }
     __syncwarp();
   } else if (warp <= kSyrkProducerWarps) {
-    // ===================== producers: compacted bits -> bytes =====================
+    // ===================== producers: compacted bits -> E2M1 nibbles =====================
     // Each thread owns A row r and B row r; the Y words of the next kAhead
     // stages are prefetched into registers (L2 latency hidden).
     const int r = threadIdx.x - 32;             // 0..127
-    const uint32_t stage_a = smem_u32(stages), stage_b = stage_a + kRows * kChunk;
+    const uint32_t row_off = (r >> 3) * (kSRowBytes / 16) * 128 + (r & 7) * 16;
+    const uint32_t stage_a = smem_u32(stages) + row_off, stage_b = stage_a + kRows * kSRowBytes;
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
@@ -300,15 +378,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             }
             mbar_wait(&empty_bar[st], ph ^ 1);
             if (!(s.debug_skip & 2)) {
-              expand_quad(stage_a + st * kStageBytes, r, 0, a0);
-              expand_quad(stage_a + st * kStageBytes, r, 1, a1);
-              expand_quad(stage_b + st * kStageBytes, r, 0, b0);
-              expand_quad(stage_b + st * kStageBytes, r, 1, b1);
+              const uint32_t so = st * kSStageBytes;
+              expand_quad_f4(stage_a + so, 0, a0);
+              expand_quad_f4(stage_a + so, 1, a1);
+              expand_quad_f4(stage_b + so, 0, b0);
+              expand_quad_f4(stage_b + so, 1, b1);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&full_bar[st]);
-            if (++st == kStages) { st = 0; ph ^= 1; }
+            if (++st == kSStages) { st = 0; ph ^= 1; }
           }
         }
         wk.next(s);
@@ -336,49 +415,45 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
+      uint32_t u = 0;
       for (uint64_t it = it0; it < it1; ++it) {
-        const uint32_t t2 = uint32_t(it - it0);
         const IInfo inf = s.info[wk.ii];
         const uint32_t i = s.i_lo + wk.ii;
-        // ---- phase a = 0: TMEM -> scratch
-        mbar_wait_sleep(&tfull_bar[0], t2 & 1);
-        fence_after();
-        for (int m = 0; m < kRounds; ++m) {
-          uint32_t v0[8], v1[8];
-          const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + 8 * (half * kRounds + m);
-          tmem_ld8(taddr, v0);
-          tmem_ld8(taddr + 128, v1);
-          tmem_wait_ld();
+        // ---- drain the four units (a, c) of this tile: TMEM (f32 counts) ->
+        // u32 scratch, releasing each ring slot at once so the MMAs of the
+        // next units overlap the scoring below.
 #pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            scr[(m * 16 + x) * 256] = inf.q[0][0] ? v0[x] : 0u;
-            scr[(m * 16 + 8 + x) * 256] = inf.q[0][1] ? v1[x] : 0u;
-          }
-        }
-        fence_before();
-        mbar_arrive(&tempty_bar[0]);
-        // ---- phase a = 1: TMEM -> scratch, then release TMEM before scoring, so
-        // the K2 work of this tile overlaps the next tile's MMAs.
-        mbar_wait_sleep(&tfull_bar[1], t2 & 1);
-        fence_after();
-        for (int m = 0; m < kRounds; ++m) {
-          uint32_t v0[8], v1[8];
-          const uint32_t taddr =
-              tmem + (uint32_t(quarter * 32) << 16) + 256 + 8 * (half * kRounds + m);
-          tmem_ld8(taddr, v0);
-          tmem_ld8(taddr + 128, v1);
-          tmem_wait_ld();
+        for (uint32_t a = 0; a < 2; ++a)
 #pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            scr[(kRounds * 16 + m * 16 + x) * 256] = inf.q[1][0] ? v0[x] : 0u;
-            scr[(kRounds * 16 + m * 16 + 8 + x) * 256] = inf.q[1][1] ? v1[x] : 0u;
+          for (uint32_t c = 0; c < 2; ++c, ++u) {
+            const uint32_t slot = u % kUnits;
+            mbar_wait_sleep(&tfull_bar[slot], (u / kUnits) & 1);
+            fence_after();
+            const bool nonempty = inf.q[a][c] != 0;
+            const uint32_t taddr =
+                tmem + (uint32_t(quarter * 32) << 16) + slot * 128 + half * 8 * kRounds;
+#pragma unroll
+            for (int m2 = 0; m2 < kRounds; m2 += 2) {
+              uint32_t v[16];
+              tmem_ld16(taddr + 8 * m2, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int x = 0; x < 16; ++x) {
+                const int m = m2 + (x >> 3);
+                scr[(a * kRounds * 16 + m * 16 + c * 8 + (x & 7)) * 256] =
+                    nonempty ? f32_count(v[x]) : 0u;
+              }
+            }
+            fence_before();
+            mbar_arrive(&tempty_bar[slot]);
           }
-        }
-        fence_before();
-        mbar_arrive(&tempty_bar[1]);
         const uint32_t j = i + 1 + wk.jb * kJB + jl;
         const uint32_t jc = min(j, M - 1);
         const uint64_t gth = *reinterpret_cast<volatile uint64_t*>(s.gthr);
+        // screening bound: a triple whose fp32 screen exceeds thr_f cannot reach
+        // the threshold (margin proven on the host, k2_screen_margin)
+        const float thr_f = gth == ~0ull ? __int_as_float(0x7f800000)
+                                         : __double2float_ru(key_score(gth) + d.kshift);
         uint64_t rank_ij = 0;
         if (kRanged) {
           const uint64_t Mi = M - i, Mj = M - jc;
@@ -399,8 +474,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             v1[x] = scr[(kRounds * 16 + m * 16 + 8 + x) * 256];
           }
           // This thread holds T_a[b=bsel][g] for k phases t=0..3 (index 2t+g),
-          // a=0 in u (scratch), a=1 in v (TMEM). Thread b owns phases 2b, 2b+1;
-          // it sends the partner (b^1) its values for the partner's phases.
+          // a=0 in u, a=1 in v. Thread b owns phases 2b, 2b+1; it sends the
+          // partner (b^1) its values for the partner's phases.
           uint32_t snd[16], rcv[16];
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
@@ -449,8 +524,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               derive_cells(T1, pij1, __ldg(d.pair[1] + size_t(i) * M + kc),
                            __ldg(d.pair[1] + size_t(jc) * M + kc), si1, sj1,
                            __ldg(d.single[1] + kc), d.n[1], n1);
-              sk = score_key(k2_device(n0, n1, d.logp));
-              tk = triple_key(i, j, k);
+              if (!s.screen || k2_screen(n0, n1, ktab) <= thr_f) {
+                sk = score_key(k2_device(n0, n1, d.logp));
+                tk = triple_key(i, j, k);
+              }
             }
             const bool want = valid && sk <= gth &&
                               (nlist < K || key_less(sk, tk, ls[K - 1], lt[K - 1]));
