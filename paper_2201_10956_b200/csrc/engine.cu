@@ -94,7 +94,7 @@ struct DevData {
   uint32_t n[2];             // class sample counts N0, N1
   const uint4* planes[2];    // [wq][M][2]
   const uint2* single[2];    // [M]: popc(plane0), popc(plane1)
-  const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y)
+  const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y), mirrored at [y*M+x]
   const double* logp;        // build_log_table(N+1): N+2 entries
   const uint64_t* itemoff;   // [M-1] prefix item counts per i
   const float* ktab;         // screening table G[n] = fl32(logp[n] - alpha*n), ktab_n entries
@@ -168,13 +168,15 @@ __device__ __forceinline__ double k2_device(const uint32_t* n0, const uint32_t* 
 // screen passes the current threshold are scored exactly with k2_device.
 __device__ __forceinline__ float k2_screen(const uint32_t* n0, const uint32_t* n1,
                                            const float* G) {
-  float s = 0.f;
+  // three independent partial sums (shorter dependency chain); the margin
+  // bound holds for any summation order
+  float s[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int c = 0; c < 27; ++c) {
     const uint32_t r0 = n0[c], r1 = n1[c];
-    s = __fadd_rn(s, __fsub_rn(__fsub_rn(G[r0 + r1 + 1], G[r0]), G[r1]));
+    s[c % 3] = __fadd_rn(s[c % 3], __fsub_rn(__fsub_rn(G[r0 + r1 + 1], G[r0]), G[r1]));
   }
-  return s;
+  return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
 }
 
 // One 32-sample word of one class for one (i, j, k): 8 AND3 + 8 POPC.
@@ -531,7 +533,13 @@ __global__ void pairs_kernel(const uint4* __restrict__ planes, uint32_t M, uint3
     c10 += __popc(x1.x & y0.x) + __popc(x1.y & y0.y) + __popc(x1.z & y0.z) + __popc(x1.w & y0.w);
     c11 += __popc(x1.x & y1.x) + __popc(x1.y & y1.y) + __popc(x1.z & y1.z) + __popc(x1.w & y1.w);
   }
-  if (y > x && y < M) pair[size_t(x) * M + y] = make_uint4(c00, c01, c10, c11);
+  if (y > x && y < M) {
+    // both triangles hold the (x<y) counts, so pair[k*M + j] (j<k) gives warps
+    // whose lanes walk consecutive j a contiguous row
+    const uint4 v = make_uint4(c00, c01, c10, c11);
+    pair[size_t(x) * M + y] = v;
+    pair[size_t(y) * M + x] = v;
+  }
 }
 
 // Per-triple tables / scores through the same marginal derivation as the search.

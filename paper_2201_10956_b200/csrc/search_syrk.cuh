@@ -489,10 +489,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           }
 #pragma unroll
           for (int x = 0; x < 16; ++x) rcv[x] = __shfl_xor_sync(0xffffffffu, snd[x], 1);
+          // The two k phases this thread owns, interleaved stage by stage so the
+          // independent load and screening chains of both triples overlap.
+          uint32_t T[2][2][8];  // [h][class][a*4 + b*2 + g]
+          uint32_t kk[2];
+          bool valid[2];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {  // the two k phases this thread owns
-            const int tt = 2 * bsel + h;
-            uint32_t T0[8], T1[8];
+          for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
               const int o0 = 2 * h + g, o1 = 2 * (2 + h) + g;  // own index for bsel 0 / 1
@@ -502,37 +505,61 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
               for (int bb = 0; bb < 2; ++bb) {
                 const bool mine = bb == bsel;
-                T0[0 * 4 + bb * 2 + g] = mine ? own_u0 : rcv[px];
-                T1[0 * 4 + bb * 2 + g] = mine ? own_u1 : rcv[4 + px];
-                T0[1 * 4 + bb * 2 + g] = mine ? own_v0 : rcv[8 + px];
-                T1[1 * 4 + bb * 2 + g] = mine ? own_v1 : rcv[12 + px];
+                T[h][0][0 * 4 + bb * 2 + g] = mine ? own_u0 : rcv[px];
+                T[h][1][0 * 4 + bb * 2 + g] = mine ? own_u1 : rcv[4 + px];
+                T[h][0][1 * 4 + bb * 2 + g] = mine ? own_v0 : rcv[8 + px];
+                T[h][1][1 * 4 + bb * 2 + g] = mine ? own_v1 : rcv[12 + px];
               }
             }
-            const uint32_t k = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + tt;
-            const uint32_t kc = min(k, M - 1);
-            bool valid = j < k && k < M && !(s.debug_skip & 1);
-            if (kRanged && valid) {
-              const uint64_t rr = rank_ij + (k - j - 1);
-              valid = rr >= s.rank_begin && rr < s.rank_end;
+            kk[h] = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h;
+            valid[h] = j < kk[h] && kk[h] < M && !(s.debug_skip & 1);
+            if (kRanged && valid[h]) {
+              const uint64_t rr = rank_ij + (kk[h] - j - 1);
+              valid[h] = rr >= s.rank_begin && rr < s.rank_end;
             }
-            uint64_t sk = ~0ull, tk = ~0ull;
-            if (valid) {
+          }
+          uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
+          if (valid[0] || valid[1]) {
+            uint4 pik[2][2], pjk[2][2];
+            uint2 skc[2][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t kc = min(kk[h], M - 1);
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                pik[h][c] = __ldg(d.pair[c] + size_t(i) * M + kc);
+                pjk[h][c] = __ldg(d.pair[c] + size_t(kc) * M + jc);
+                skc[h][c] = __ldg(d.single[c] + kc);
+              }
+            }
+            bool pass[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
               uint32_t n0[27], n1[27];
-              derive_cells(T0, pij0, __ldg(d.pair[0] + size_t(i) * M + kc),
-                           __ldg(d.pair[0] + size_t(jc) * M + kc), si0, sj0,
-                           __ldg(d.single[0] + kc), d.n[0], n0);
-              derive_cells(T1, pij1, __ldg(d.pair[1] + size_t(i) * M + kc),
-                           __ldg(d.pair[1] + size_t(jc) * M + kc), si1, sj1,
-                           __ldg(d.single[1] + kc), d.n[1], n1);
-              if (!s.screen || k2_screen(n0, n1, ktab) <= thr_f) {
-                sk = score_key(k2_device(n0, n1, d.logp));
-                tk = triple_key(i, j, k);
+              derive_cells(T[h][0], pij0, pik[h][0], pjk[h][0], si0, sj0, skc[h][0], d.n[0], n0);
+              derive_cells(T[h][1], pij1, pik[h][1], pjk[h][1], si1, sj1, skc[h][1], d.n[1], n1);
+              if (s.debug_skip & 4)
+                pass[h] = n0[26] == 0x7fffffffu;  // profiling: derivation only
+              else
+                pass[h] = valid[h] && (!s.screen || k2_screen(n0, n1, ktab) <= thr_f);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (pass[h]) {  // rare once the threshold has settled: score exactly
+                uint32_t n0[27], n1[27];
+                derive_cells(T[h][0], pij0, pik[h][0], pjk[h][0], si0, sj0, skc[h][0], d.n[0], n0);
+                derive_cells(T[h][1], pij1, pik[h][1], pjk[h][1], si1, sj1, skc[h][1], d.n[1], n1);
+                sk[h] = score_key(k2_device(n0, n1, d.logp));
+                tk[h] = triple_key(i, j, kk[h]);
               }
             }
-            const bool want = valid && sk <= gth &&
-                              (nlist < K || key_less(sk, tk, ls[K - 1], lt[K - 1]));
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const bool want = valid[h] && sk[h] <= gth &&
+                              (nlist < K || key_less(sk[h], tk[h], ls[K - 1], lt[K - 1]));
             const unsigned cand = __ballot_sync(0xffffffffu, want);
-            if (cand) warp_insert(ls, lt, nlist, K, cand, sk, tk, lane, s.gthr);
+            if (cand) warp_insert(ls, lt, nlist, K, cand, sk[h], tk[h], lane, s.gthr);
           }
         }
         wk.next(s);
