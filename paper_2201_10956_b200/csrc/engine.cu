@@ -599,6 +599,7 @@ struct e3_dataset {
   int num_sms = 0, search_ctas_per_sm = 0, search_min_blocks = 1;
   size_t smem_optin = 0;
   uint32_t debug_skip = 0;  // E3_DEBUG_SKIP (profiling experiments only)
+  bool no_drop = false;     // E3_SYRK_NO_DROP: always compute phases 0 and 1 (A/B testing)
   // scratch reused across searches
   ulonglong2* lists[2] = {nullptr, nullptr};
   uint32_t* counts[2] = {nullptr, nullptr};
@@ -795,6 +796,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
                                 int(tc::smem_bytes(E3_MAX_TOP_K))));
   ds->smem_optin = prop.sharedMemPerBlockOptin;
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
+  ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
@@ -912,13 +914,20 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
       inf.R = uint32_t(2 * (M - 1 - i));
       inf.nb = uint32_t((M - 1 - i + syrk::kJB - 1) / syrk::kJB);
       size_t ysz = 0;
-      for (int a = 0; a < 2; ++a)
-        for (int c = 0; c < 2; ++c) {
-          const uint2 sc = ds->h_single[c][i];
-          inf.n[a][c] = a == 0 ? sc.x : sc.y;
-          inf.q[a][c] = (inf.n[a][c] + 255) / 256 * 2;
-          ysz += size_t(inf.q[a][c]) * inf.R;
+      for (int c = 0; c < 2; ++c) {
+        // genotype counts of SNP i in class c; the largest phase is dropped
+        const uint2 sc = ds->h_single[c][i];
+        const uint64_t g[3] = {sc.x, sc.y, ds->N[c] - sc.x - sc.y};
+        const uint32_t drop = g[2] >= g[0] && g[2] >= g[1] ? 2u : (g[1] >= g[0] ? 1u : 0u);
+        inf.drop[c] = ds->no_drop ? 2u : drop;
+        for (int p = 0, a = 0; a < 3; ++a) {
+          if (uint32_t(a) == inf.drop[c]) continue;
+          inf.n[p][c] = uint32_t(g[a]);
+          inf.q[p][c] = (inf.n[p][c] + 255) / 256 * 2;
+          ysz += size_t(inf.q[p][c]) * inf.R;
+          ++p;
         }
+      }
       if (bt.n > 0 && bt.ytot + ysz > kYBudget) break;
       for (int a = 0; a < 2; ++a) {
         inf.y_off[a] = bt.ytot;

@@ -90,12 +90,16 @@ constexpr int kSyrkThreads = 32 * (1 + kSyrkProducerWarps + kEpilogueWarps);
 
 // Per-i layout of the compacted operands (one record per i of the batch).
 struct IInfo {
-  uint64_t y_off[2];     // uint4 offset of Y_{i,a} in the batch buffer
-  uint64_t pos_off[2][2];// u32 offset of S_{i,a,c} in the position buffer
-  uint32_t n[2][2];      // |S_{i,a,c}|
-  uint32_t q[2][2];      // quads of class c in Y_{i,a} (even: 256-sample stages)
+  // Per class c only two of the three genotype phases of SNP i are computed
+  // ("slots" p = 0, 1: phases lo < hi); the largest phase drop[c] follows
+  // exactly from the pair index: T_drop[b][g] = P_jk[b][g] - T_lo - T_hi.
+  uint64_t y_off[2];     // uint4 offset of Y_{i,p} (slot p, both classes) in the batch buffer
+  uint64_t pos_off[2][2];// u32 offset of S_{i,phase(p,c),c} in the position buffer
+  uint32_t n[2][2];      // |S_{i,phase(p,c),c}|
+  uint32_t q[2][2];      // quads of class c in Y_{i,p} (even: 256-sample stages)
   uint32_t R;            // rows = 2 (M - 1 - i)
   uint32_t nb;           // 64-SNP blocks above i
+  uint32_t drop[2];      // dropped phase per class (slots hold the other two, ascending)
 };
 
 struct SyrkArgs {
@@ -117,10 +121,13 @@ struct SyrkArgs {
 // S_{i,a,c}: block-wide exclusive scan of popcounts over the class words of X_a^i.
 __global__ void __launch_bounds__(1024) compact_positions_kernel(const DevData d, SyrkArgs s,
                                                                 uint32_t* __restrict__ pos) {
-  const uint32_t ii = blockIdx.x, a = blockIdx.y, c = blockIdx.z;
+  const uint32_t ii = blockIdx.x, p = blockIdx.y, c = blockIdx.z;
   const uint32_t i = s.i_lo + ii;
   const IInfo inf = s.info[ii];
-  uint32_t* out = pos + inf.pos_off[a][c];
+  uint32_t* out = pos + inf.pos_off[p][c];
+  // slot p holds phase: p + (p >= drop) skipping the dropped one
+  const uint32_t a = (p == 0) ? (inf.drop[c] == 0 ? 1u : 0u) : (inf.drop[c] == 2 ? 1u : 2u);
+  const uint32_t ncls = d.n[c];
   const uint32_t nw = d.wq[c] * 4;
   const uint4* pl = c ? d.planes[1] : d.planes[0];
   const size_t row = size_t(d.M) * 2;
@@ -132,9 +139,18 @@ __global__ void __launch_bounds__(1024) compact_positions_kernel(const DevData d
     const uint32_t w = w0 + threadIdx.x;
     uint32_t bits = 0;
     if (w < nw) {
-      const uint4 q = __ldg(pl + size_t(w >> 2) * row + 2 * i + a);
-      const uint32_t comp[4] = {q.x, q.y, q.z, q.w};
-      bits = comp[w & 3];
+      if (a < 2) {
+        const uint4 q = __ldg(pl + size_t(w >> 2) * row + 2 * i + a);
+        const uint32_t comp[4] = {q.x, q.y, q.z, q.w};
+        bits = comp[w & 3];
+      } else {  // genotype 2 = NOT(g0 | g1) on the class's valid samples
+        const uint4 q0 = __ldg(pl + size_t(w >> 2) * row + 2 * i);
+        const uint4 q1 = __ldg(pl + size_t(w >> 2) * row + 2 * i + 1);
+        const uint32_t c0[4] = {q0.x, q0.y, q0.z, q0.w}, c1[4] = {q1.x, q1.y, q1.z, q1.w};
+        const uint32_t lo = w * 32;
+        const uint32_t valid = lo >= ncls ? 0u : (ncls - lo >= 32 ? ~0u : ((1u << (ncls - lo)) - 1u));
+        bits = ~(c0[w & 3] | c1[w & 3]) & valid;
+      }
     }
     const uint32_t cnt = __popc(bits);
     // block exclusive scan of cnt
@@ -530,6 +546,23 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 pik[h][c] = __ldg(d.pair[c] + size_t(i) * M + kc);
                 pjk[h][c] = __ldg(d.pair[c] + size_t(kc) * M + jc);
                 skc[h][c] = __ldg(d.single[c] + kc);
+              }
+              // slots -> phases 0 and 1; the dropped phase from the pair index
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const uint32_t P[4] = {pjk[h][c].x, pjk[h][c].y, pjk[h][c].z, pjk[h][c].w};
+                uint32_t* t = T[h][c];
+                if (inf.drop[c] == 1) {
+#pragma unroll
+                  for (int x = 0; x < 4; ++x) t[4 + x] = P[x] - t[x] - t[4 + x];
+                } else if (inf.drop[c] == 0) {
+#pragma unroll
+                  for (int x = 0; x < 4; ++x) {
+                    const uint32_t t1 = t[x];
+                    t[x] = P[x] - t[x] - t[4 + x];
+                    t[4 + x] = t1;
+                  }
+                }
               }
             }
             bool pass[2];
