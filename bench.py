@@ -153,14 +153,14 @@ def main():
     ap.add_argument("--slices", type=int, default=64,
                     help="a step searches 1/SLICES of the triple-rank space per GPU")
     ap.add_argument("--engine", default="auto", choices=["auto", "syrk", "tc_masked", "popc"],
-                    help="auto (default): syrk for N >= 8192 else tc_masked; syrk: compacted "
-                         "tcgen05 kind::i8 SYRK; tc_masked: tcgen05 GEMM over pair products; "
+                    help="auto (default): syrk for N >= 4096 else tc_masked; syrk: compacted "
+                         "tcgen05 kind::mxf4 SYRK; tc_masked: tcgen05 GEMM over pair products; "
                          "popc: LOP3/POPC kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.engine == "auto":
-        args.engine = "syrk" if WORKLOADS[args.workload][1] >= 8192 else "tc_masked"
+        args.engine = "syrk" if WORKLOADS[args.workload][1] >= 4096 else "tc_masked"
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
 
@@ -210,10 +210,15 @@ def main():
     syrk_macs = 0.0
     snp_ones = None
     if args.engine == "syrk":
-        # per-SNP count of samples with genotype 0 or 1 (both classes)
+        # per SNP i: compacted samples the SYRK engine multiplies = per class the
+        # two smaller genotype phases of i (the largest is recovered exactly)
         def popc64(x):
             return np.unpackbits(x.view(np.uint8), axis=-1).sum(axis=-1, dtype=np.int64)
-        snp_ones = (popc64(ds.ctrl).sum(axis=1) + popc64(ds.cases).sum(axis=1)).astype(np.float64)
+        snp_ones = np.zeros(M, dtype=np.float64)
+        for planes, n_c in ((ds.ctrl, ds.num_controls), (ds.cases, ds.num_cases)):
+            g = popc64(planes)                      # [M, 2]: genotype 0, 1 counts
+            g3 = np.stack([g[:, 0], g[:, 1], n_c - g[:, 0] - g[:, 1]], axis=1)
+            snp_ones += (n_c - g3.max(axis=1)).astype(np.float64)
         ii = np.arange(M, dtype=np.float64)
         c3 = lambda n: n * (n - 1) * (n - 2) / 6.0
         first_rank = c3(float(M)) - c3(M - ii)
@@ -286,19 +291,22 @@ def main():
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
             if (ROOT / "MEASURED_PEAKS.json").exists() else {}
         if args.engine in ("syrk", "tc_masked"):
+            bf16 = peaks.get("bf16_tflops", 1590.0)
             if args.engine == "tc_masked":
                 # masked GEMM: 8 int8 MACs (16 ops) per triplet x sample
                 achieved = kernel_rate * TC_OPS_PER_ELEMENT / 1e12
+                peak, kind = 2.0 * bf16, "int8"  # dense int8 = 2x dense bf16 on B200
             else:
-                # compacted SYRK: 4 MACs per (triple, compacted sample), exact count
+                # compacted SYRK: 4 fp4 MACs per (triple, compacted sample), exact count
                 achieved = 2.0 * syrk_macs / (kern_ms / 1e3) / 1e12
-            bf16 = peaks.get("bf16_tflops", 1590.0)
-            peak = 2.0 * bf16  # dense int8 = 2x dense bf16 on B200
-            roof = {"bound": "tensor", "unit": "TOPS (int8, algorithmic)",
-                    "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (burst)" if peaks
-                                    else "2 x fallback 1590 TFLOP/s"),
-                    "note": ("compacted SYRK: 4 int8 MACs per triple per sample where SNP i "
-                             "has genotype 0 or 1 (exact count over the timed slices)"
+                peak, kind = 4.0 * bf16, "fp4"   # dense fp4 (kind::mxf4) = 4x dense bf16
+            mult = 2 if kind == "int8" else 4
+            roof = {"bound": "tensor", "unit": f"TFLOP/s ({kind} dense, algorithmic)",
+                    "peak_source": (f"{mult} x MEASURED_PEAKS.json bf16_tflops (burst)" if peaks
+                                    else f"{mult} x fallback 1590 TFLOP/s"),
+                    "note": ("compacted SYRK: 4 fp4 MACs per triple per compacted sample, i.e. "
+                             "per sample in the two smaller genotype phases of SNP i per class "
+                             "(exact count over the timed slices)"
                              if args.engine == "syrk" else
                              "masked GEMM: 8 int8 MACs per element (4 (a,b) pair rows x 2 g "
                              "columns)") + "; the other cells come exactly from the marginal "
@@ -327,8 +335,10 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": ("u8 (0/1 int8 MMA, s32 accumulate) + f64 (K2)" if args.engine != "popc"
-                      else "u32 (bit-plane LOP3/POPC) + f64 (K2)"),
+            "vs_baseline": None,
+            "dtype": {"syrk": "e2m1 (0/1 fp4 MMA, exact f32 accumulate) + f64 (K2)",
+                      "tc_masked": "u8 (0/1 int8 MMA, s32 accumulate) + f64 (K2)",
+                      "popc": "u32 (bit-plane LOP3/POPC) + f64 (K2)"}[args.engine],
             "data": "synthetic",
             "config": {"workload": desc, "top_k": top_k,
                        "step": f"one search over a 1/{args.slices} triple-rank slice "

@@ -63,7 +63,7 @@ typedef struct {
 
 #define E3_MAX_TOP_K 256u
 /* Engine selection (e3_search_cfg.flags). All engines produce identical
- * results; 0 = auto (E3_ENGINE_SYRK for N >= 8192 samples, else
+ * results; 0 = auto (E3_ENGINE_SYRK for N >= 4096 samples, else
  * E3_ENGINE_TC_MASKED).
  *   E3_ENGINE_POPC       LOP3/POPC kernel (marginal subtraction + carry-save)
  *   E3_ENGINE_TC_MASKED  tcgen05 kind::i8 GEMM: pair products x singles

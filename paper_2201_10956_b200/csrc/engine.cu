@@ -1062,7 +1062,7 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   // the SYRK engine accumulates exact counts in f32 (fp4 operands): N_c < 2^23
   const bool syrk_ok = std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 23);
   if (engine == 0)  // auto: compaction pays off once the sample axis is long
-    engine = (ds->N[0] + ds->N[1]) >= 8192 && syrk_ok ? E3_ENGINE_SYRK : E3_ENGINE_TC_MASKED;
+    engine = (ds->N[0] + ds->N[1]) >= 4096 && syrk_ok ? E3_ENGINE_SYRK : E3_ENGINE_TC_MASKED;
   if (engine == E3_ENGINE_SYRK && !syrk_ok)
     return fail(E3_DOMAIN, "the SYRK engine supports at most 2^23 - 1 samples per class");
   const bool use_syrk = engine == E3_ENGINE_SYRK;
