@@ -166,15 +166,22 @@ __device__ __forceinline__ double k2_device(const uint32_t* n0, const uint32_t* 
 // per cell up to the constant alpha, so score = screen + 27*alpha up to an
 // error the host bounds rigorously (k2_screen_margin); only triples whose
 // screen passes the current threshold are scored exactly with k2_device.
-__device__ __forceinline__ float k2_screen(const uint32_t* n0, const uint32_t* n1,
-                                           const float* G) {
+__device__ __forceinline__ float lds_f32(uint32_t saddr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
+  return v;
+}
+// G_s: shared-memory (32-bit) address of the table.
+__device__ __forceinline__ float k2_screen(const uint32_t* n0, const uint32_t* n1, uint32_t G_s) {
   // three independent partial sums (shorter dependency chain); the margin
   // bound holds for any summation order
   float s[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int c = 0; c < 27; ++c) {
     const uint32_t r0 = n0[c], r1 = n1[c];
-    s[c % 3] = __fadd_rn(s[c % 3], __fsub_rn(__fsub_rn(G[r0 + r1 + 1], G[r0]), G[r1]));
+    const float t = __fsub_rn(__fsub_rn(lds_f32(G_s + 4 * (r0 + r1 + 1)), lds_f32(G_s + 4 * r0)),
+                              lds_f32(G_s + 4 * r1));
+    s[c % 3] = __fadd_rn(s[c % 3], t);
   }
   return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
 }

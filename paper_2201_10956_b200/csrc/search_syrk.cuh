@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base_sh;
+  const uint32_t ktab_s = smem_u32(ktab);
   // Block scale factors = 1.0 (UE8M0 0x7F) in columns [kSfCol, kSfCol+32) of
   // all 128 lanes: one epilogue warp per TMEM lane quarter writes them.
   if (warp > kSyrkProducerWarps && warp <= kSyrkProducerWarps + 4) {
@@ -574,7 +575,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               if (s.debug_skip & 4)
                 pass[h] = n0[26] == 0x7fffffffu;  // profiling: derivation only
               else
-                pass[h] = valid[h] && (!s.screen || k2_screen(n0, n1, ktab) <= thr_f);
+                pass[h] = valid[h] && (!s.screen || k2_screen(n0, n1, ktab_s) <= thr_f);
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
