@@ -900,6 +900,11 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
              uint32_t i_first, uint32_t i_last, uint32_t grid, uint32_t* launches) {
   const uint64_t M = ds->M;
   cudaStream_t st = ds->stream;
+  // lexicographic rank of the first triple with first SNP i: C(M,3) - C(M-i,3)
+  auto first_rank = [M](uint64_t i) {
+    auto c3 = [](uint64_t n) { return n < 3 ? 0 : n * (n - 1) / 2 * (n - 2) / 3; };
+    return c3(M) - c3(M - i);
+  };
   constexpr size_t kYBudget = size_t(3) << 20;   // uint4 elements per batch (48 MiB)
   struct Batch {
     uint32_t first, n, rmax, qmax;
@@ -1019,7 +1024,11 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     if (bt.qmax > 0)
       syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0, st>>>(
           d, sa, ds->pos_buf, ds->y_buf);
-    if (ranged) syrk::search_syrk_kernel<true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    // only batches holding a partially covered first SNP need per-triple rank
+    // checks; the others run the unranged kernel
+    const uint64_t b_lo = first_rank(bt.first), b_hi = first_rank(bt.first + bt.n);
+    const bool part = ranged && (r0 > b_lo || r1 < b_hi);
+    if (part) syrk::search_syrk_kernel<true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     else syrk::search_syrk_kernel<false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     CUDA_TRY(cudaGetLastError());
     *launches += 3;

@@ -25,7 +25,8 @@ from typing import Iterable, Optional, Sequence
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "libepi3cu.so"
+# E3_LIBCU: path of an alternative build of the same library (A/B experiments)
+_LIB_PATH = Path(os.environ.get("E3_LIBCU") or Path(__file__).resolve().parent / "libepi3cu.so")
 
 # ---------------------------------------------------------------------------
 # errors: the epi3::Error hierarchy (common.hpp:36-105)
