@@ -433,6 +433,7 @@ search_kernel(const DevData d, const SearchArgs a) {
 
 #include "search_tc.cuh"
 #include "search_syrk.cuh"
+#include "pairs_tc.cuh"
 
 namespace {
 
@@ -523,32 +524,6 @@ __global__ void singles_kernel(const uint4* __restrict__ planes, uint32_t M, uin
 }
 
 // pair[x*M + y] for x < y: {popc(X0x&X0y), popc(X0x&X1y), popc(X1x&X0y), popc(X1x&X1y)}.
-__global__ void pairs_kernel(const uint4* __restrict__ planes, uint32_t M, uint32_t wq,
-                             uint4* __restrict__ pair) {
-  const uint32_t x = blockIdx.y;
-  const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.x * blockDim.x + blockDim.x <= x + 1) return;  // whole block below diagonal
-  const uint32_t yc = min(y, M - 1);
-  uint32_t c00 = 0, c01 = 0, c10 = 0, c11 = 0;
-  const size_t row = size_t(M) * 2;
-  const uint4* p = planes;
-  for (uint32_t w = 0; w < wq; ++w, p += row) {
-    const uint4 x0 = __ldg(p + 2 * x), x1 = __ldg(p + 2 * x + 1);
-    const uint4 y0 = __ldg(p + 2 * yc), y1 = __ldg(p + 2 * yc + 1);
-    c00 += __popc(x0.x & y0.x) + __popc(x0.y & y0.y) + __popc(x0.z & y0.z) + __popc(x0.w & y0.w);
-    c01 += __popc(x0.x & y1.x) + __popc(x0.y & y1.y) + __popc(x0.z & y1.z) + __popc(x0.w & y1.w);
-    c10 += __popc(x1.x & y0.x) + __popc(x1.y & y0.y) + __popc(x1.z & y0.z) + __popc(x1.w & y0.w);
-    c11 += __popc(x1.x & y1.x) + __popc(x1.y & y1.y) + __popc(x1.z & y1.z) + __popc(x1.w & y1.w);
-  }
-  if (y > x && y < M) {
-    // both triangles hold the (x<y) counts, so pair[k*M + j] (j<k) gives warps
-    // whose lanes walk consecutive j a contiguous row
-    const uint4 v = make_uint4(c00, c01, c10, c11);
-    pair[size_t(x) * M + y] = v;
-    pair[size_t(y) * M + x] = v;
-  }
-}
-
 // Per-triple tables / scores through the same marginal derivation as the search.
 __global__ void triples_kernel(const DevData d, const uint32_t* __restrict__ triples, uint64_t n,
                                uint32_t* __restrict__ tables, double* __restrict__ scores) {
@@ -701,6 +676,17 @@ double k2_screen_margin(double gmax, double N, double alpha) {
 }
 
 int build(e3_dataset* ds, const uint64_t* host[2]) {
+  // E3_TRACE_CREATE=1: per-phase wall times of dataset creation on stderr
+  const bool trace = std::getenv("E3_TRACE_CREATE") != nullptr;
+  auto tlast = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    if (ds->stream) cudaStreamSynchronize(ds->stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[create] %-12s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tlast).count());
+    tlast = now;
+  };
   CUDA_TRY(cudaSetDevice(ds->device));
   {
     cudaMemPool_t pool;
@@ -711,9 +697,13 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
   for (auto& e : ds->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaEventCreateWithFlags(&ds->ev_upload, cudaEventDisableTiming));
-  cudaDeviceProp prop;
-  CUDA_TRY(cudaGetDeviceProperties(&prop, ds->device));
-  ds->num_sms = prop.multiProcessorCount;
+  mark("stream");
+  // two attributes only: cudaGetDeviceProperties costs 10-35 ms per call
+  int n_sms = 0, smem_optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, ds->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ds->device));
+  mark("props");
+  ds->num_sms = n_sms;
   const uint32_t M = uint32_t(ds->M);
   uint32_t* bad = nullptr;
   CUDA_TRY(dmalloc(ds, &bad, sizeof(uint32_t)));
@@ -730,8 +720,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     CUDA_TRY(cudaMemsetAsync(ds->planes[c], 0, plane_bytes, ds->stream));
     if (ds->wq[c] == 0) {
       CUDA_TRY(cudaMemsetAsync(ds->single[c], 0, sizeof(uint2) * M, ds->stream));
-      CUDA_TRY(cudaMemsetAsync(ds->pair[c], 0, sizeof(uint4) * size_t(M) * M, ds->stream));
-      continue;
+      continue;  // pairs_tc_kernel writes the (all-zero) pair index
     }
     uint64_t* raw = nullptr;
     const size_t raw_bytes = sizeof(uint64_t) * size_t(M) * 2 * w64;
@@ -744,12 +733,29 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
         raw, M, w64, ds->wq[c], tail, ds->planes[c], bad);
     singles_kernel<<<(M + 255) / 256, 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
                                                           ds->single[c]);
-    pairs_kernel<<<dim3((M + 255) / 256, M), 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
-                                                                 ds->pair[c]);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaStreamSynchronize(ds->stream));
     dfree(ds, raw);
   }
+  mark("planes");
+  {
+    // marginal pair index of both classes: one tensor-core Gram launch
+    pairs_tc::PArgs pa{};
+    pa.M = M;
+    pa.nb = (M + pairs_tc::kBlk - 1) / pairs_tc::kBlk;
+    pa.units = 2ull * pa.nb * (pa.nb + 1) / 2;
+    for (int c = 0; c < 2; ++c) {
+      pa.wq[c] = ds->wq[c];
+      pa.planes[c] = ds->planes[c];
+      pa.pair[c] = ds->pair[c];
+    }
+    CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(pairs_tc::smem_bytes())));
+    const uint32_t grid = uint32_t(std::min<uint64_t>(ds->num_sms, pa.units));
+    pairs_tc::pairs_tc_kernel<<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
+    CUDA_TRY(cudaGetLastError());
+  }
+  mark("pairs");
   for (int c = 0; c < 2; ++c) {
     ds->h_single[c].resize(M);
     CUDA_TRY(cudaMemcpyAsync(ds->h_single[c].data(), ds->single[c], sizeof(uint2) * M,
@@ -801,7 +807,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaFuncSetAttribute(tc::search_tc_kernel<true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(tc::smem_bytes(E3_MAX_TOP_K))));
-  ds->smem_optin = prop.sharedMemPerBlockOptin;
+  ds->smem_optin = size_t(smem_optin);
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false>,
@@ -811,6 +817,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
+  mark("tables");
   uint32_t h_bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
   CUDA_TRY(cudaStreamSynchronize(ds->stream));
@@ -842,6 +849,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_kernel<false, 1>,
                                                            kWarps * 32, list_smem));
   ds->search_ctas_per_sm = std::max(1, occ);
+  mark("finish");
   return E3_OK;
 }
 

@@ -1,0 +1,221 @@
+// pairs_tc.cuh — the marginal pair index as a tensor-core Gram matrix
+// (included by engine.cu after search_syrk.cuh; reuses its fp4 helpers).
+//
+// pair[c][x*M + y] = {popc(X0^x & X0^y), popc(X0^x & X1^y), popc(X1^x & X0^y),
+// popc(X1^x & X1^y)} over class c, for x < y, mirrored at [y*M + x]. With the
+// plane rows (snp, g) as operand rows this is G_c = X_c X_c^T: per tile of
+// 64 x-SNPs by 64 y-SNPs (x-block <= y-block) and class, one 128 x 128 f32
+// accumulator over the class's samples, issued as tcgen05.mma kind::mxf4 on
+// E2M1 0/1 nibbles (exact: counts < 2^23). Replaces the POPC pairs_kernel
+// (15.6 ms at 8192 x 16384) in dataset creation.
+//
+// Warp roles: warp 0 issues the MMAs, warps 1-4 expand plane quads into the
+// fp4 stages (thread r owns A row r and B row r), warps 5-8 drain TMEM and
+// write both triangles of the index.
+
+namespace pairs_tc {
+
+using namespace tc;
+using syrk::kSChunk;
+using syrk::kSRowBytes;
+using syrk::kSStageBytes;
+using syrk::kSfCol;
+
+constexpr int kStagesP = 4;
+constexpr int kProd = 4, kDrain = 4;
+constexpr int kThreadsP = 32 * (1 + kProd + kDrain);
+constexpr int kBlk = 64;  // SNPs per block -> 128 operand rows
+
+struct PArgs {
+  uint32_t M, nb;           // SNPs, 64-SNP blocks
+  uint32_t wq[2];           // word-quads per class
+  const uint4* planes[2];   // [wq + 1][M][2]
+  uint4* pair[2];           // [M * M]
+  uint64_t units;           // 2 classes x nb (nb + 1) / 2 tiles
+};
+
+// unit -> (class, x-block, y-block), class-major, row-major triangle xb <= yb
+struct PWalker {
+  uint32_t c, xb, yb, nb;
+  __device__ void start(const PArgs& p, uint64_t u) {
+    nb = p.nb;
+    const uint64_t per = uint64_t(nb) * (nb + 1) / 2;
+    c = uint32_t(u / per);
+    uint64_t r = u % per;
+    xb = 0;
+    while (r >= uint64_t(nb - xb)) { r -= nb - xb; ++xb; }
+    yb = xb + uint32_t(r);
+  }
+  __device__ void next() {
+    if (++yb == nb) {
+      if (++xb == nb) { xb = 0; ++c; }
+      yb = xb;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[kStagesP], empty_bar[kStagesP];
+  __shared__ uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t u0 = p.units * blockIdx.x / gridDim.x;
+  const uint64_t u1 = p.units * (blockIdx.x + 1) / gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStagesP; ++st) {
+      mbar_init(&full_bar[st], kProd);
+      mbar_init(&empty_bar[st], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 32 * kDrain);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)), "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  if (warp > kProd) {  // block scale factors = 1.0, one warp per TMEM lane quarter
+    const uint32_t addr = tmem + (uint32_t((warp & 3) * 32) << 16) + kSfCol;
+    const uint32_t one = 0x7F7F7F7Fu;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
+        "r"(one)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+
+  if (warp == 0) {
+    if (lane == 0 && u0 < u1) {
+      PWalker wk;
+      wk.start(p, u0);
+      uint32_t n = 0;
+      const uint32_t tsf = tmem + kSfCol;
+      for (uint64_t u = u0; u < u1; ++u) {
+        const uint32_t t = uint32_t(u - u0), slot = t & 1;
+        mbar_wait(&tempty_bar[slot], ((t >> 1) & 1) ^ 1);
+        fence_after();
+        const uint32_t nch = (p.wq[wk.c] + 1) / 2;
+        const uint32_t dcol = tmem + slot * 128;
+        for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
+          const uint32_t st = n % kStagesP;
+          mbar_wait_spin(&full_bar[st], (n / kStagesP) & 1);
+          fence_after();
+          const uint32_t abase = smem_u32(stages + st * kSStageBytes);
+          const uint32_t bbase = abase + kRows * kSRowBytes;
+#pragma unroll
+          for (int kk = 0; kk < kSRowBytes / 32; ++kk)
+            syrk::mma_f4(dcol, syrk::f4_desc(abase + kk * 256), syrk::f4_desc(bbase + kk * 256), tsf,
+                         (ch != 0 || kk != 0) ? 1u : 0u);
+          mma_commit(&empty_bar[st]);
+        }
+        mma_commit(&tfull_bar[slot]);
+        wk.next();
+      }
+    }
+    __syncwarp();
+  } else if (warp <= kProd) {
+    const int r = threadIdx.x - 32;  // 0..127
+    const uint32_t row_off = (r >> 3) * (kSRowBytes / 16) * 128 + (r & 7) * 16;
+    const uint32_t stage_a = smem_u32(stages) + row_off, stage_b = stage_a + kRows * kSRowBytes;
+    if (u0 < u1) {
+      PWalker wk;
+      wk.start(p, u0);
+      uint32_t st = 0, ph = 0;
+      const uint32_t rmax = 2 * p.M - 1;
+      for (uint64_t u = u0; u < u1; ++u) {
+        const size_t row = size_t(p.M) * 2;
+        const uint4* pl = p.planes[wk.c];
+        const uint4* Ya = pl + min(2 * kBlk * wk.xb + r, rmax);
+        const uint4* Yb = pl + min(2 * kBlk * wk.yb + r, rmax);
+        const uint32_t nq = (p.wq[wk.c] + 1) / 2 * 2;  // zero quad pads an odd count
+        uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
+        if (nq) {
+          a0 = __ldg(Ya); a1 = __ldg(Ya + row);
+          b0 = __ldg(Yb); b1 = __ldg(Yb + row);
+        }
+        for (uint32_t q = 0; q < nq; q += 2) {
+          const uint4 ca0 = a0, ca1 = a1, cb0 = b0, cb1 = b1;
+          if (q + 2 < nq) {
+            const size_t o = size_t(q + 2) * row;
+            a0 = __ldg(Ya + o); a1 = __ldg(Ya + o + row);
+            b0 = __ldg(Yb + o); b1 = __ldg(Yb + o + row);
+          }
+          mbar_wait(&empty_bar[st], ph ^ 1);
+          const uint32_t so = st * kSStageBytes;
+          syrk::expand_quad_f4(stage_a + so, 0, ca0);
+          syrk::expand_quad_f4(stage_a + so, 1, ca1);
+          syrk::expand_quad_f4(stage_b + so, 0, cb0);
+          syrk::expand_quad_f4(stage_b + so, 1, cb1);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full_bar[st]);
+          if (++st == kStagesP) { st = 0; ph ^= 1; }
+        }
+        wk.next();
+      }
+    }
+  } else {
+    // drain: lane = row (x, a); columns (y, b) -> uint2 {b=0, b=1} at
+    // component offset 2a of pair[x*M + y] and of the mirror pair[y*M + x]
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int a = row & 1;
+    if (u0 < u1) {
+      PWalker wk;
+      wk.start(p, u0);
+      for (uint64_t u = u0; u < u1; ++u) {
+        const uint32_t t = uint32_t(u - u0), slot = t & 1;
+        mbar_wait_sleep(&tfull_bar[slot], (t >> 1) & 1);
+        fence_after();
+        const uint32_t x = wk.xb * kBlk + (row >> 1);
+        const bool empty = p.wq[wk.c] == 0;
+        uint32_t* base = reinterpret_cast<uint32_t*>(p.pair[wk.c]);
+        const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + slot * 128;
+#pragma unroll 1
+        for (int c16 = 0; c16 < 128; c16 += 16) {
+          uint32_t v[16];
+          syrk::tmem_ld16(taddr + c16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t y = wk.yb * kBlk + (c16 >> 1) + e;
+            if (x < y && y < p.M) {
+              const uint2 w = empty ? make_uint2(0u, 0u)
+                                    : make_uint2(syrk::f32_count(v[2 * e]), syrk::f32_count(v[2 * e + 1]));
+              *reinterpret_cast<uint2*>(base + (size_t(x) * p.M + y) * 4 + 2 * a) = w;
+              *reinterpret_cast<uint2*>(base + (size_t(y) * p.M + x) * 4 + 2 * a) = w;
+            }
+          }
+        }
+        fence_before();
+        mbar_arrive(&tempty_bar[slot]);
+        wk.next();
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  }
+}
+
+inline size_t smem_bytes() { return 1024 + size_t(kStagesP) * kSStageBytes; }
+
+}  // namespace pairs_tc
