@@ -525,6 +525,34 @@ __global__ void singles_kernel(const uint4* __restrict__ planes, uint32_t M, uin
 
 // pair[x*M + y] for x < y: {popc(X0x&X0y), popc(X0x&X1y), popc(X1x&X0y), popc(X1x&X1y)}.
 // Per-triple tables / scores through the same marginal derivation as the search.
+// POPC pair index, used only when a class holds >= 2^23 samples (beyond the
+// exact f32 range of pairs_tc_kernel).
+__global__ void pairs_kernel(const uint4* __restrict__ planes, uint32_t M, uint32_t wq,
+                             uint4* __restrict__ pair) {
+  const uint32_t x = blockIdx.y;
+  const uint32_t y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x * blockDim.x + blockDim.x <= x + 1) return;  // whole block below diagonal
+  const uint32_t yc = min(y, M - 1);
+  uint32_t c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+  const size_t row = size_t(M) * 2;
+  const uint4* p = planes;
+  for (uint32_t w = 0; w < wq; ++w, p += row) {
+    const uint4 x0 = __ldg(p + 2 * x), x1 = __ldg(p + 2 * x + 1);
+    const uint4 y0 = __ldg(p + 2 * yc), y1 = __ldg(p + 2 * yc + 1);
+    c00 += __popc(x0.x & y0.x) + __popc(x0.y & y0.y) + __popc(x0.z & y0.z) + __popc(x0.w & y0.w);
+    c01 += __popc(x0.x & y1.x) + __popc(x0.y & y1.y) + __popc(x0.z & y1.z) + __popc(x0.w & y1.w);
+    c10 += __popc(x1.x & y0.x) + __popc(x1.y & y0.y) + __popc(x1.z & y0.z) + __popc(x1.w & y0.w);
+    c11 += __popc(x1.x & y1.x) + __popc(x1.y & y1.y) + __popc(x1.z & y1.z) + __popc(x1.w & y1.w);
+  }
+  if (y > x && y < M) {
+    // both triangles hold the (x<y) counts, so pair[k*M + j] (j<k) gives warps
+    // whose lanes walk consecutive j a contiguous row
+    const uint4 v = make_uint4(c00, c01, c10, c11);
+    pair[size_t(x) * M + y] = v;
+    pair[size_t(y) * M + x] = v;
+  }
+}
+
 __global__ void triples_kernel(const DevData d, const uint32_t* __restrict__ triples, uint64_t n,
                                uint32_t* __restrict__ tables, double* __restrict__ scores) {
   const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -752,7 +780,13 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(pairs_tc::smem_bytes())));
     const uint32_t grid = uint32_t(std::min<uint64_t>(ds->num_sms, pa.units));
-    pairs_tc::pairs_tc_kernel<<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
+    if (std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 23)) {
+      pairs_tc::pairs_tc_kernel<<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
+    } else {
+      for (int c = 0; c < 2; ++c)
+        pairs_kernel<<<dim3((M + 255) / 256, M), 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
+                                                                     ds->pair[c]);
+    }
     CUDA_TRY(cudaGetLastError());
   }
   mark("pairs");

@@ -198,3 +198,24 @@ def test_engines_agree_on_random_inputs():
             b = dd.search(epi3.SearchConfig(top_k=33, engine="popc"))
             c = dd.search(epi3.SearchConfig(top_k=33, engine="tc_masked"))
         assert epi3.same_outcome(a, b) and epi3.same_outcome(a, c), (M, n0, n1)
+
+
+def test_class_beyond_exact_f32_range():
+    """A class of >= 2^23 samples: the pair index falls back to POPC, auto
+    picks the s32-accumulating masked engine, and SYRK refuses loudly."""
+    n0, n1, M = (1 << 23) + 3, 64, 5
+    rng = np.random.default_rng(11)
+    geno = rng.integers(0, 3, (M, n0 + n1), dtype=np.uint8)
+    pheno = np.zeros(n0 + n1, dtype=np.uint8)
+    pheno[rng.choice(n0 + n1, n1, replace=False)] = 1
+    ds = epi3.binarize(geno, pheno)
+    od = po.OracleDataset.of(ds)
+    triples = [(a, b, c) for a in range(M) for b in range(a + 1, M) for c in range(b + 1, M)]
+    with epi3.DeviceDataset(ds) as dd:
+        tabs = dd.tables(triples)
+        got = hits_of(dd.search(epi3.SearchConfig(top_k=4)))
+        with pytest.raises(epi3.DomainError):
+            dd.search(epi3.SearchConfig(top_k=4, engine="syrk"))
+    for t, tab in zip(triples, tabs):
+        assert (tab == od.table(t)).all(), t
+    assert_hits_identical(got, od.search(top_k=4))
