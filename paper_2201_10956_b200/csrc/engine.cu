@@ -618,6 +618,10 @@ struct e3_dataset {
   uint64_t* gthr = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_upload = nullptr;
+  // SYRK compaction runs on its own stream, one batch ahead of the search
+  // kernel (double-buffered Y / positions); the events order the two
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_cdone[2] = {nullptr, nullptr}, ev_sdone[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -653,6 +657,14 @@ void release(e3_dataset* ds) {
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
   if (ds->ev_upload) cudaEventDestroy(ds->ev_upload);
+  for (int b = 0; b < 2; ++b) {
+    if (ds->ev_cdone[b]) cudaEventDestroy(ds->ev_cdone[b]);
+    if (ds->ev_sdone[b]) cudaEventDestroy(ds->ev_sdone[b]);
+  }
+  if (ds->cstream) {
+    cudaStreamSynchronize(ds->cstream);
+    cudaStreamDestroy(ds->cstream);
+  }
   if (ds->stream) {
     cudaStreamSynchronize(ds->stream);
     cudaStreamDestroy(ds->stream);
@@ -725,6 +737,11 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
   for (auto& e : ds->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaEventCreateWithFlags(&ds->ev_upload, cudaEventDisableTiming));
+  CUDA_TRY(cudaStreamCreateWithFlags(&ds->cstream, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ds->ev_cdone[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ds->ev_sdone[b], cudaEventDisableTiming));
+  }
   mark("stream");
   // two attributes only: cudaGetDeviceProperties costs 10-35 ms per call
   int n_sms = 0, smem_optin = 0;
@@ -1009,13 +1026,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   if (ymax > ds->y_cap) {
     dfree(ds, ds->y_buf);
     ds->y_buf = nullptr;
-    CUDA_TRY(dmalloc(ds, &ds->y_buf, sizeof(uint4) * std::max<size_t>(ymax, 1)));
+    CUDA_TRY(dmalloc(ds, &ds->y_buf, 2 * sizeof(uint4) * std::max<size_t>(ymax, 1)));
     ds->y_cap = ymax;
   }
   if (pmax > ds->pos_cap) {
     dfree(ds, ds->pos_buf);
     ds->pos_buf = nullptr;
-    CUDA_TRY(dmalloc(ds, &ds->pos_buf, sizeof(uint32_t) * std::max<size_t>(pmax, 1)));
+    CUDA_TRY(dmalloc(ds, &ds->pos_buf, 2 * sizeof(uint32_t) * std::max<size_t>(pmax, 1)));
     ds->pos_cap = pmax;
   }
   const size_t info_need = infos.size() + offs.size();
@@ -1044,7 +1061,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   const bool screen = tsm + sizeof(float) * ds->ktab_n <= ds->smem_optin - 2048 &&
                       !std::getenv("E3_NO_SCREEN");
   if (screen) tsm += sizeof(float) * ds->ktab_n;
-  for (const Batch& bt : batches) {
+  // compaction waits for the metadata upload (and all earlier work on st)
+  CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_upload, 0));
+  for (size_t b = 0; b < batches.size(); ++b) {
+    const Batch& bt = batches[b];
+    const int buf = int(b & 1);
+    uint4* ybuf = ds->y_buf + size_t(buf) * ds->y_cap;
+    uint32_t* pbuf = ds->pos_buf + size_t(buf) * ds->pos_cap;
     syrk::SyrkArgs sa{};
     sa.item_begin = 0;
     sa.item_count = bt.tiles;
@@ -1058,14 +1081,19 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.counts = ds->counts[0];
     sa.info = ds->info_buf + bt.info_at;
     sa.itemoff = ds->syrk_off + bt.off_at;
-    sa.Y = ds->y_buf;
+    sa.Y = ybuf;
     sa.scratch = ds->scratch;
     sa.debug_skip = ds->debug_skip;
     sa.screen = screen ? 1u : 0u;
-    syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, st>>>(d, sa, ds->pos_buf);
+    // batch b's compaction overlaps batch b-1's search; it may reuse buffer
+    // b & 1 only once batch b-2's search is done with it
+    if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_sdone[buf], 0));
+    syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, ds->cstream>>>(d, sa, pbuf);
     if (bt.qmax > 0)
-      syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0, st>>>(
-          d, sa, ds->pos_buf, ds->y_buf);
+      syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0,
+                                    ds->cstream>>>(d, sa, pbuf, ybuf);
+    CUDA_TRY(cudaEventRecord(ds->ev_cdone[buf], ds->cstream));
+    CUDA_TRY(cudaStreamWaitEvent(st, ds->ev_cdone[buf], 0));
     // only batches holding a partially covered first SNP need per-triple rank
     // checks; the others run the unranged kernel
     const uint64_t b_lo = first_rank(bt.first), b_hi = first_rank(bt.first + bt.n);
@@ -1073,6 +1101,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     if (part) syrk::search_syrk_kernel<true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     else syrk::search_syrk_kernel<false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(ds->ev_sdone[buf], st));
     *launches += 3;
   }
   // the host vectors die here: wait for their uploads only (kernels keep running)
