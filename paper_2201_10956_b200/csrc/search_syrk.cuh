@@ -482,6 +482,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
         const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
         for (int m = 0; m < kRounds; ++m) {
+          // pair(j,k) rows first: their L2 latency overlaps the scratch loads
+          // and the lane-pair exchange below
+          uint4 pjk[2][2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const size_t o = size_t(min(i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h,
+                                        M - 1)) * M + jc;
+            pjk[h][0] = __ldg(d.pair[0] + o);
+            pjk[h][1] = __ldg(d.pair[1] + o);
+          }
           uint32_t v0[8], v1[8], u0[8], u1[8];
 #pragma unroll
           for (int x = 0; x < 8; ++x) {
@@ -537,7 +547,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           }
           uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
           if (valid[0] || valid[1]) {
-            uint4 pik[2][2], pjk[2][2];
+            uint4 pik[2][2];
             uint2 skc[2][2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -545,7 +555,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
               for (int c = 0; c < 2; ++c) {
                 pik[h][c] = __ldg(d.pair[c] + size_t(i) * M + kc);
-                pjk[h][c] = __ldg(d.pair[c] + size_t(kc) * M + jc);
                 skc[h][c] = __ldg(d.single[c] + kc);
               }
               // slots -> phases 0 and 1; the dropped phase from the pair index
