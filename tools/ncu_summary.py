@@ -34,6 +34,10 @@ KEYS = [
     ("l1tex__t_sector_hit_rate.pct", "L1 hit rate"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum", "tensor-core shared-memory wavefronts"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1TEX throughput % of peak"),
+    ("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+     "tensor (hmma/fp4) subpipe % of peak"),
     ("smsp__inst_executed.sum", "warp instructions"),
 ]
 
