@@ -94,7 +94,9 @@ struct DevData {
   uint32_t n[2];             // class sample counts N0, N1
   const uint4* planes[2];    // [wq][M][2]
   const uint2* single[2];    // [M]: popc(plane0), popc(plane1)
-  const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y), mirrored at [y*M+x]
+  const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y); mirrored at
+                             // [y*M+x] unless `pairn` holds the (narrow) mirror
+  const uint2* pairn[2];     // [M*M] u16 counts {00|01<<16, 10|11<<16}, both triangles (N_c < 2^16)
   const double* logp;        // build_log_table(N+1): N+2 entries
   const uint64_t* itemoff;   // [M-1] prefix item counts per i
   const float* ktab;         // screening table G[n] = fl32(logp[n] - alpha*n), ktab_n entries
@@ -588,6 +590,8 @@ struct e3_dataset {
   uint4* planes[2] = {nullptr, nullptr};
   uint2* single[2] = {nullptr, nullptr};
   uint4* pair[2] = {nullptr, nullptr};
+  uint2* pairn[2] = {nullptr, nullptr};  // narrow mirrored pair index (every N_c < 2^16)
+  bool narrow = false;
   double* logp = nullptr;
   float* ktab = nullptr;              // K2 screening table (see k2_screen)
   uint32_t ktab_n = 0;
@@ -641,6 +645,7 @@ void release(e3_dataset* ds) {
     dfree(ds, ds->planes[c]);
     dfree(ds, ds->single[c]);
     dfree(ds, ds->pair[c]);
+    dfree(ds, ds->pairn[c]);
     dfree(ds, ds->lists[c]);
     dfree(ds, ds->counts[c]);
   }
@@ -691,6 +696,7 @@ DevData dev_view(const e3_dataset* ds) {
     d.planes[c] = ds->planes[c];
     d.single[c] = ds->single[c];
     d.pair[c] = ds->pair[c];
+    d.pairn[c] = ds->pairn[c];
   }
   d.logp = ds->logp;
   d.itemoff = ds->itemoff;
@@ -750,6 +756,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   mark("props");
   ds->num_sms = n_sms;
   const uint32_t M = uint32_t(ds->M);
+  ds->narrow = std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 16) && !std::getenv("E3_NO_NARROW");
   uint32_t* bad = nullptr;
   CUDA_TRY(dmalloc(ds, &bad, sizeof(uint32_t)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), ds->stream));
@@ -759,6 +766,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     ds->wq[c] = uint32_t((n + 127) / 128);
     CUDA_TRY(dmalloc(ds, &ds->single[c], sizeof(uint2) * M));
     CUDA_TRY(dmalloc(ds, &ds->pair[c], sizeof(uint4) * size_t(M) * M));
+    if (ds->narrow) CUDA_TRY(dmalloc(ds, &ds->pairn[c], sizeof(uint2) * size_t(M) * M));
     // one extra zero quad: the search kernel steps two quads at a time
     const size_t plane_bytes = sizeof(uint4) * (size_t(ds->wq[c]) + 1) * M * 2;
     CUDA_TRY(dmalloc(ds, &ds->planes[c], plane_bytes));
@@ -792,13 +800,20 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
       pa.wq[c] = ds->wq[c];
       pa.planes[c] = ds->planes[c];
       pa.pair[c] = ds->pair[c];
+      pa.pairn[c] = ds->pairn[c];
     }
-    CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel,
+    CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(pairs_tc::smem_bytes())));
+    CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(pairs_tc::smem_bytes())));
     const uint32_t grid = uint32_t(std::min<uint64_t>(ds->num_sms, pa.units));
     if (std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 23)) {
-      pairs_tc::pairs_tc_kernel<<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
+      if (ds->narrow)
+        pairs_tc::pairs_tc_kernel<true><<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
+      else
+        pairs_tc::pairs_tc_kernel<false><<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
     } else {
       for (int c = 0; c < 2; ++c)
         pairs_kernel<<<dim3((M + 255) / 256, M), 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
@@ -861,10 +876,16 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   ds->smem_optin = size_t(smem_optin);
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false>,
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true>,
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 2048)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 2048)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
@@ -1098,8 +1119,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     // checks; the others run the unranged kernel
     const uint64_t b_lo = first_rank(bt.first), b_hi = first_rank(bt.first + bt.n);
     const bool part = ranged && (r0 > b_lo || r1 < b_hi);
-    if (part) syrk::search_syrk_kernel<true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
-    else syrk::search_syrk_kernel<false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    if (ds->narrow) {
+      if (part) syrk::search_syrk_kernel<true, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    } else {
+      if (part) syrk::search_syrk_kernel<true, false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ds->ev_sdone[buf], st));
     *launches += 3;

@@ -30,7 +30,8 @@ struct PArgs {
   uint32_t M, nb;           // SNPs, 64-SNP blocks
   uint32_t wq[2];           // word-quads per class
   const uint4* planes[2];   // [wq + 1][M][2]
-  uint4* pair[2];           // [M * M]
+  uint4* pair[2];           // [M * M] wide (u32) counts
+  uint2* pairn[2];          // [M * M] narrow (u16) mirror, when every class < 2^16 samples
   uint64_t units;           // 2 classes x nb (nb + 1) / 2 tiles
 };
 
@@ -54,6 +55,9 @@ struct PWalker {
   }
 };
 
+// kNarrow: the wide index gets the upper triangle only (what the other
+// engines read) and the SYRK engine's mirrored index is written narrow.
+template <bool kNarrow>
 __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -198,7 +202,14 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
               const uint2 w = empty ? make_uint2(0u, 0u)
                                     : make_uint2(syrk::f32_count(v[2 * e]), syrk::f32_count(v[2 * e + 1]));
               *reinterpret_cast<uint2*>(base + (size_t(x) * p.M + y) * 4 + 2 * a) = w;
-              *reinterpret_cast<uint2*>(base + (size_t(y) * p.M + x) * 4 + 2 * a) = w;
+              if (kNarrow) {
+                uint32_t* nb = reinterpret_cast<uint32_t*>(p.pairn[wk.c]);
+                const uint32_t h = w.x | (w.y << 16);
+                nb[(size_t(x) * p.M + y) * 2 + a] = h;
+                nb[(size_t(y) * p.M + x) * 2 + a] = h;
+              } else {
+                *reinterpret_cast<uint2*>(base + (size_t(y) * p.M + x) * 4 + 2 * a) = w;
+              }
             }
           }
         }

@@ -250,7 +250,9 @@ struct SWalker {
   }
 };
 
-template <bool kRanged>
+// kNarrow: every class has < 2^16 samples, so pair(j,k) comes from the
+// 8-byte mirrored index d.pairn (u16 counts), fetched one round ahead.
+template <bool kRanged, bool kNarrow>
 __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -481,16 +483,24 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         const uint4 pij1 = __ldg(d.pair[1] + size_t(i) * M + jc);
         const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
         const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
+        const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
         for (int m = 0; m < kRounds; ++m) {
           // pair(j,k) rows first: their L2 latency overlaps the scratch loads
           // and the lane-pair exchange below
           uint4 pjk[2][2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const size_t o = size_t(min(i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h,
-                                        M - 1)) * M + jc;
-            pjk[h][0] = __ldg(d.pair[0] + o);
-            pjk[h][1] = __ldg(d.pair[1] + o);
+            const size_t o = size_t(min(kbase + 4 * m + h, M - 1)) * M + jc;
+            if (kNarrow) {
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const uint2 w = __ldg(d.pairn[c] + o);
+                pjk[h][c] = make_uint4(w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16);
+              }
+            } else {
+              pjk[h][0] = __ldg(d.pair[0] + o);
+              pjk[h][1] = __ldg(d.pair[1] + o);
+            }
           }
           uint32_t v0[8], v1[8], u0[8], u1[8];
 #pragma unroll
