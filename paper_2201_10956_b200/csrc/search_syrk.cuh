@@ -456,11 +456,21 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               uint32_t v[16];
               tmem_ld16(taddr + 8 * m2, v);
               tmem_wait_ld();
+              if constexpr (kNarrow) {
+                // u16 counts: (g=0 | g=1 << 16) of k phase t in one word
 #pragma unroll
-              for (int x = 0; x < 16; ++x) {
-                const int m = m2 + (x >> 3);
-                scr[(a * kRounds * 16 + m * 16 + c * 8 + (x & 7)) * 256] =
-                    nonempty ? f32_count(v[x]) : 0u;
+                for (int x = 0; x < 8; ++x) {
+                  const int m = m2 + (x >> 2), t = x & 3;
+                  scr[(a * kRounds * 8 + m * 8 + c * 4 + t) * 256] =
+                      nonempty ? (f32_count(v[2 * x]) | (f32_count(v[2 * x + 1]) << 16)) : 0u;
+                }
+              } else {
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                  const int m = m2 + (x >> 3);
+                  scr[(a * kRounds * 16 + m * 16 + c * 8 + (x & 7)) * 256] =
+                      nonempty ? f32_count(v[x]) : 0u;
+                }
               }
             }
             fence_before();
@@ -502,6 +512,37 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               pjk[h][1] = __ldg(d.pair[1] + o);
             }
           }
+          uint32_t T[2][2][8];  // [h][class][a*4 + b*2 + g]
+          if constexpr (kNarrow) {
+            // packed words W[unit = a*2 + c][t] = T(g=0) | T(g=1) << 16 of this
+            // row (j, b=bsel) for k phase t; the partner row (j, b^1) sends its
+            // words for this thread's phases 2*bsel + h
+            uint32_t W[4][4];
+#pragma unroll
+            for (int un = 0; un < 4; ++un)
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                W[un][t] = scr[((un >> 1) * kRounds * 8 + m * 8 + (un & 1) * 4 + t) * 256];
+            uint32_t rcv[4][2];
+#pragma unroll
+            for (int un = 0; un < 4; ++un)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                rcv[un][h] = __shfl_xor_sync(0xffffffffu, bsel ? W[un][h] : W[un][2 + h], 1);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int un = 0; un < 4; ++un) {
+                const int a = un >> 1, c = un & 1;
+                const uint32_t own = bsel ? W[un][2 + h] : W[un][h];
+#pragma unroll
+                for (int bb = 0; bb < 2; ++bb) {
+                  const uint32_t w = (bb == bsel) ? own : rcv[un][h];
+                  T[h][c][a * 4 + bb * 2 + 0] = w & 0xffffu;
+                  T[h][c][a * 4 + bb * 2 + 1] = w >> 16;
+                }
+              }
+          } else {
           uint32_t v0[8], v1[8], u0[8], u1[8];
 #pragma unroll
           for (int x = 0; x < 8; ++x) {
@@ -526,11 +567,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           }
 #pragma unroll
           for (int x = 0; x < 16; ++x) rcv[x] = __shfl_xor_sync(0xffffffffu, snd[x], 1);
-          // The two k phases this thread owns, interleaved stage by stage so the
-          // independent load and screening chains of both triples overlap.
-          uint32_t T[2][2][8];  // [h][class][a*4 + b*2 + g]
-          uint32_t kk[2];
-          bool valid[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -548,6 +584,12 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 T[h][1][1 * 4 + bb * 2 + g] = mine ? own_v1 : rcv[12 + px];
               }
             }
+          }
+          }
+          uint32_t kk[2];
+          bool valid[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
             kk[h] = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h;
             valid[h] = j < kk[h] && kk[h] < M && !(s.debug_skip & 1);
             if (kRanged && valid[h]) {
