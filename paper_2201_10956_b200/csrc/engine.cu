@@ -95,8 +95,11 @@ struct DevData {
   const uint4* planes[2];    // [wq][M][2]
   const uint2* single[2];    // [M]: popc(plane0), popc(plane1)
   const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y); mirrored at
-                             // [y*M+x] unless `pairn` holds the (narrow) mirror
-  const uint2* pairn[2];     // [M*M] u16 counts {00|01<<16, 10|11<<16}, both triangles (N_c < 2^16)
+                             // [y*M+x] unless narrow (then `pairp` holds the mirror)
+  // narrow (every N_c < 2^16): class-packed u16 counts, word = class0 | class1 << 16
+  const uint4* pairp;        // [M*M] {00, 01, 10, 11}, both triangles
+  const uint2* singlep;      // [M] {plane 0, plane 1}
+  uint32_t npk;              // N0 | N1 << 16
   const double* logp;        // build_log_table(N+1): N+2 entries
   const uint64_t* itemoff;   // [M-1] prefix item counts per i
   const float* ktab;         // screening table G[n] = fl32(logp[n] - alpha*n), ktab_n entries
@@ -163,16 +166,29 @@ __device__ __forceinline__ double k2_device(const uint32_t* n0, const uint32_t* 
 }
 
 
-// fp32 screen of k2_score: sum_c (G[r0+r1+1] - G[r0]) - G[r1] over a
-// shared-memory table G[n] = fl32(P[n] - alpha*n). The affine shift cancels
-// per cell up to the constant alpha, so score = screen + 27*alpha up to an
-// error the host bounds rigorously (k2_screen_margin); only triples whose
-// screen passes the current threshold are scored exactly with k2_device.
 __device__ __forceinline__ float lds_f32(uint32_t saddr) {
   float v;
   asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
   return v;
 }
+// k2_screen on class-packed cells (narrow path): word = class0 | class1 << 16.
+__device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_s) {
+  float s[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 27; ++c) {
+    const uint32_t r0 = n[c] & 0xffffu, r1 = n[c] >> 16;
+    const float t = __fsub_rn(__fsub_rn(lds_f32(G_s + 4 * (r0 + r1 + 1)), lds_f32(G_s + 4 * r0)),
+                              lds_f32(G_s + 4 * r1));
+    s[c % 3] = __fadd_rn(s[c % 3], t);
+  }
+  return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
+}
+
+// fp32 screen of k2_score: sum_c (G[r0+r1+1] - G[r0]) - G[r1] over a
+// shared-memory table G[n] = fl32(P[n] - alpha*n). The affine shift cancels
+// per cell up to the constant alpha, so score = screen + 27*alpha up to an
+// error the host bounds rigorously (k2_screen_margin); only triples whose
+// screen passes the current threshold are scored exactly with k2_device.
 // G_s: shared-memory (32-bit) address of the table.
 __device__ __forceinline__ float k2_screen(const uint32_t* n0, const uint32_t* n1, uint32_t G_s) {
   // three independent partial sums (shorter dependency chain); the margin
@@ -527,6 +543,15 @@ __global__ void singles_kernel(const uint4* __restrict__ planes, uint32_t M, uin
 
 // pair[x*M + y] for x < y: {popc(X0x&X0y), popc(X0x&X1y), popc(X1x&X0y), popc(X1x&X1y)}.
 // Per-triple tables / scores through the same marginal derivation as the search.
+// Class-packed single counts for the narrow SYRK path: {p0: c0 | c1 << 16, p1: ...}.
+__global__ void pack_singles_kernel(const uint2* __restrict__ s0, const uint2* __restrict__ s1,
+                                    uint32_t M, uint2* __restrict__ out) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= M) return;
+  const uint2 a = s0[x], b = s1[x];
+  out[x] = make_uint2(a.x | (b.x << 16), a.y | (b.y << 16));
+}
+
 // POPC pair index, used only when a class holds >= 2^23 samples (beyond the
 // exact f32 range of pairs_tc_kernel).
 __global__ void pairs_kernel(const uint4* __restrict__ planes, uint32_t M, uint32_t wq,
@@ -590,7 +615,8 @@ struct e3_dataset {
   uint4* planes[2] = {nullptr, nullptr};
   uint2* single[2] = {nullptr, nullptr};
   uint4* pair[2] = {nullptr, nullptr};
-  uint2* pairn[2] = {nullptr, nullptr};  // narrow mirrored pair index (every N_c < 2^16)
+  uint4* pairp = nullptr;    // narrow class-packed mirrored pair index (every N_c < 2^16)
+  uint2* singlep = nullptr;  // narrow class-packed single counts
   bool narrow = false;
   double* logp = nullptr;
   float* ktab = nullptr;              // K2 screening table (see k2_screen)
@@ -645,10 +671,12 @@ void release(e3_dataset* ds) {
     dfree(ds, ds->planes[c]);
     dfree(ds, ds->single[c]);
     dfree(ds, ds->pair[c]);
-    dfree(ds, ds->pairn[c]);
+
     dfree(ds, ds->lists[c]);
     dfree(ds, ds->counts[c]);
   }
+  dfree(ds, ds->pairp);
+  dfree(ds, ds->singlep);
   dfree(ds, ds->logp);
   dfree(ds, ds->ktab);
   dfree(ds, ds->itemoff);
@@ -696,10 +724,13 @@ DevData dev_view(const e3_dataset* ds) {
     d.planes[c] = ds->planes[c];
     d.single[c] = ds->single[c];
     d.pair[c] = ds->pair[c];
-    d.pairn[c] = ds->pairn[c];
+
   }
   d.logp = ds->logp;
   d.itemoff = ds->itemoff;
+  d.pairp = ds->pairp;
+  d.singlep = ds->singlep;
+  d.npk = uint32_t(ds->N[0]) | (uint32_t(ds->N[1]) << 16);
   d.ktab = ds->ktab;
   d.ktab_n = ds->ktab_n;
   d.kshift = ds->kshift;
@@ -766,7 +797,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     ds->wq[c] = uint32_t((n + 127) / 128);
     CUDA_TRY(dmalloc(ds, &ds->single[c], sizeof(uint2) * M));
     CUDA_TRY(dmalloc(ds, &ds->pair[c], sizeof(uint4) * size_t(M) * M));
-    if (ds->narrow) CUDA_TRY(dmalloc(ds, &ds->pairn[c], sizeof(uint2) * size_t(M) * M));
+
     // one extra zero quad: the search kernel steps two quads at a time
     const size_t plane_bytes = sizeof(uint4) * (size_t(ds->wq[c]) + 1) * M * 2;
     CUDA_TRY(dmalloc(ds, &ds->planes[c], plane_bytes));
@@ -789,6 +820,12 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     CUDA_TRY(cudaGetLastError());
     dfree(ds, raw);
   }
+  if (ds->narrow) {
+    CUDA_TRY(dmalloc(ds, &ds->pairp, sizeof(uint4) * size_t(M) * M));
+    CUDA_TRY(dmalloc(ds, &ds->singlep, sizeof(uint2) * M));
+    pack_singles_kernel<<<(M + 255) / 256, 256, 0, ds->stream>>>(ds->single[0], ds->single[1], M,
+                                                                ds->singlep);
+  }
   mark("planes");
   {
     // marginal pair index of both classes: one tensor-core Gram launch
@@ -796,11 +833,12 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     pa.M = M;
     pa.nb = (M + pairs_tc::kBlk - 1) / pairs_tc::kBlk;
     pa.units = 2ull * pa.nb * (pa.nb + 1) / 2;
+    pa.pairp = ds->pairp;
     for (int c = 0; c < 2; ++c) {
       pa.wq[c] = ds->wq[c];
       pa.planes[c] = ds->planes[c];
       pa.pair[c] = ds->pair[c];
-      pa.pairn[c] = ds->pairn[c];
+
     }
     CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,

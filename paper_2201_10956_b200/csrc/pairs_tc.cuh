@@ -31,7 +31,7 @@ struct PArgs {
   uint32_t wq[2];           // word-quads per class
   const uint4* planes[2];   // [wq + 1][M][2]
   uint4* pair[2];           // [M * M] wide (u32) counts
-  uint2* pairn[2];          // [M * M] narrow (u16) mirror, when every class < 2^16 samples
+  uint4* pairp;             // [M * M] narrow class-packed mirror (c0 | c1 << 16), every N_c < 2^16
   uint64_t units;           // 2 classes x nb (nb + 1) / 2 tiles
 };
 
@@ -202,11 +202,14 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
               const uint2 w = empty ? make_uint2(0u, 0u)
                                     : make_uint2(syrk::f32_count(v[2 * e]), syrk::f32_count(v[2 * e + 1]));
               *reinterpret_cast<uint2*>(base + (size_t(x) * p.M + y) * 4 + 2 * a) = w;
-              if (kNarrow) {
-                uint32_t* nb = reinterpret_cast<uint32_t*>(p.pairn[wk.c]);
-                const uint32_t h = w.x | (w.y << 16);
-                nb[(size_t(x) * p.M + y) * 2 + a] = h;
-                nb[(size_t(y) * p.M + x) * 2 + a] = h;
+              if (kNarrow) {  // u16 halves: class c of components (a, b=0), (a, b=1)
+                uint16_t* nb = reinterpret_cast<uint16_t*>(p.pairp);
+                const size_t o1 = (size_t(x) * p.M + y) * 8 + a * 4 + wk.c;
+                const size_t o2 = (size_t(y) * p.M + x) * 8 + a * 4 + wk.c;
+                nb[o1] = uint16_t(w.x);
+                nb[o1 + 2] = uint16_t(w.y);
+                nb[o2] = uint16_t(w.x);
+                nb[o2 + 2] = uint16_t(w.y);
               } else {
                 *reinterpret_cast<uint2*>(base + (size_t(y) * p.M + x) * 4 + 2 * a) = w;
               }

@@ -250,8 +250,11 @@ struct SWalker {
   }
 };
 
-// kNarrow: every class has < 2^16 samples, so pair(j,k) comes from the
-// 8-byte mirrored index d.pairn (u16 counts), fetched one round ahead.
+// kNarrow: every class has < 2^16 samples, so counts are carried as
+// class-packed u16 pairs (class0 | class1 << 16) — scratch, pair index,
+// singles — and the dropped-phase recovery and the table derivation run on
+// both classes at once (every intermediate is a true count, so the packed
+// 32-bit arithmetic never carries or borrows across the halves).
 template <bool kRanged, bool kNarrow>
 __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -457,12 +460,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               tmem_ld16(taddr + 8 * m2, v);
               tmem_wait_ld();
               if constexpr (kNarrow) {
-                // u16 counts: (g=0 | g=1 << 16) of k phase t in one word
+                // u16 half c of word (a, m, t, g)
+                uint16_t* scr16 = reinterpret_cast<uint16_t*>(scr);
 #pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                  const int m = m2 + (x >> 2), t = x & 3;
-                  scr[(a * kRounds * 8 + m * 8 + c * 4 + t) * 256] =
-                      nonempty ? (f32_count(v[2 * x]) | (f32_count(v[2 * x + 1]) << 16)) : 0u;
+                for (int x = 0; x < 16; ++x) {
+                  const int m = m2 + (x >> 3), tg = x & 7;
+                  scr16[(a * kRounds * 8 + m * 8 + tg) * 512 + c] =
+                      nonempty ? uint16_t(f32_count(v[x])) : uint16_t(0);
                 }
               } else {
 #pragma unroll
@@ -489,172 +493,237 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           rank_ij = (uint64_t(M) * (M - 1) * (M - 2) - Mi * (Mi - 1) * (Mi - 2)) / 6 +
                     (uint64_t(Mi - 1) * (Mi - 2)) / 2 - Mj * (Mj - 1) / 2;
         }
-        const uint4 pij0 = __ldg(d.pair[0] + size_t(i) * M + jc);
-        const uint4 pij1 = __ldg(d.pair[1] + size_t(i) * M + jc);
-        const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
-        const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
-        const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
-        for (int m = 0; m < kRounds; ++m) {
-          // pair(j,k) rows first: their L2 latency overlaps the scratch loads
-          // and the lane-pair exchange below
-          uint4 pjk[2][2];
+        if constexpr (kNarrow) {
+          // class-packed words (class0 | class1 << 16) throughout
+          const uint4 pij = __ldg(d.pairp + size_t(i) * M + jc);
+          const uint2 sip = __ldg(d.singlep + i), sjp = __ldg(d.singlep + jc);
+          // per-half masks of the dropped phase (slots hold the other two, ascending)
+          const uint32_t mk0 = (inf.drop[0] == 0 ? 0xffffu : 0u) | (inf.drop[1] == 0 ? 0xffff0000u : 0u);
+          const uint32_t mk1 = (inf.drop[0] == 1 ? 0xffffu : 0u) | (inf.drop[1] == 1 ? 0xffff0000u : 0u);
+          const uint32_t mk2 = ~(mk0 | mk1);
+          const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
+          for (int m = 0; m < kRounds; ++m) {
+            uint4 pjk[2];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const size_t o = size_t(min(kbase + 4 * m + h, M - 1)) * M + jc;
-            if (kNarrow) {
+            for (int h = 0; h < 2; ++h)
+              pjk[h] = __ldg(d.pairp + size_t(min(kbase + 4 * m + h, M - 1)) * M + jc);
+            // W[a][t][g]: this row (j, b=bsel), unit slot a, k phase t, genotype g
+            uint32_t W[2][4][2];
 #pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                const uint2 w = __ldg(d.pairn[c] + o);
-                pjk[h][c] = make_uint4(w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16);
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int g = 0; g < 2; ++g) W[a][t][g] = scr[(a * kRounds * 8 + m * 8 + t * 2 + g) * 256];
+            // the partner row (j, b^1) sends its words for this thread's phases 2*bsel + h
+            uint32_t rcv[2][2][2];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+                  rcv[a][h][g] = __shfl_xor_sync(0xffffffffu, bsel ? W[a][h][g] : W[a][2 + h][g], 1);
+            uint32_t kk[2];
+            bool valid[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              kk[h] = kbase + 4 * m + h;
+              valid[h] = j < kk[h] && kk[h] < M && !(s.debug_skip & 1);
+              if (kRanged && valid[h]) {
+                const uint64_t rr = rank_ij + (kk[h] - j - 1);
+                valid[h] = rr >= s.rank_begin && rr < s.rank_end;
               }
-            } else {
+            }
+            uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
+            if (valid[0] || valid[1]) {
+              uint32_t T[2][8];  // [h][a*4 + b*2 + g], class-packed
+              uint4 pik[2];
+              uint2 skp[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint32_t kc = min(kk[h], M - 1);
+                pik[h] = __ldg(d.pairp + size_t(i) * M + kc);
+                skp[h] = __ldg(d.singlep + kc);
+                const uint32_t P[4] = {pjk[h].x, pjk[h].y, pjk[h].z, pjk[h].w};
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                  for (int g = 0; g < 2; ++g) {
+                    const uint32_t own0 = bsel ? W[0][2 + h][g] : W[0][h][g];
+                    const uint32_t own1 = bsel ? W[1][2 + h][g] : W[1][h][g];
+                    const uint32_t s0 = (b == bsel) ? own0 : rcv[0][h][g];
+                    const uint32_t s1 = (b == bsel) ? own1 : rcv[1][h][g];
+                    // slots -> phases 0 and 1; the dropped phase from the pair index
+                    const uint32_t X = P[b * 2 + g] - s0 - s1;
+                    T[h][b * 2 + g] = (X & mk0) | (s0 & ~mk0);
+                    T[h][4 + b * 2 + g] = (s1 & mk2) | (X & mk1) | (s0 & mk0);
+                  }
+              }
+              bool pass[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                uint32_t n[27];
+                derive_cells(T[h], pij, pik[h], pjk[h], sip, sjp, skp[h], d.npk, n);
+                if (s.debug_skip & 4)
+                  pass[h] = n[26] == 0x7fffffffu;  // profiling: derivation only
+                else
+                  pass[h] = valid[h] && (!s.screen || k2_screen_packed(n, ktab_s) <= thr_f);
+              }
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (pass[h]) {  // rare once the threshold has settled: score exactly
+                  uint32_t n[27], n0[27], n1[27];
+                  derive_cells(T[h], pij, pik[h], pjk[h], sip, sjp, skp[h], d.npk, n);
+#pragma unroll
+                  for (int c = 0; c < 27; ++c) {
+                    n0[c] = n[c] & 0xffffu;
+                    n1[c] = n[c] >> 16;
+                  }
+                  sk[h] = score_key(k2_device(n0, n1, d.logp));
+                  tk[h] = triple_key(i, j, kk[h]);
+                }
+              }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const bool want = valid[h] && sk[h] <= gth &&
+                                (nlist < K || key_less(sk[h], tk[h], ls[K - 1], lt[K - 1]));
+              const unsigned cand = __ballot_sync(0xffffffffu, want);
+              if (cand) warp_insert(ls, lt, nlist, K, cand, sk[h], tk[h], lane, s.gthr);
+            }
+          }
+        } else {
+          const uint4 pij0 = __ldg(d.pair[0] + size_t(i) * M + jc);
+          const uint4 pij1 = __ldg(d.pair[1] + size_t(i) * M + jc);
+          const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
+          const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
+          const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
+          for (int m = 0; m < kRounds; ++m) {
+            // pair(j,k) rows first: their L2 latency overlaps the scratch loads
+            // and the lane-pair exchange below
+            uint4 pjk[2][2];
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const size_t o = size_t(min(kbase + 4 * m + h, M - 1)) * M + jc;
               pjk[h][0] = __ldg(d.pair[0] + o);
               pjk[h][1] = __ldg(d.pair[1] + o);
             }
-          }
-          uint32_t T[2][2][8];  // [h][class][a*4 + b*2 + g]
-          if constexpr (kNarrow) {
-            // packed words W[unit = a*2 + c][t] = T(g=0) | T(g=1) << 16 of this
-            // row (j, b=bsel) for k phase t; the partner row (j, b^1) sends its
-            // words for this thread's phases 2*bsel + h
-            uint32_t W[4][4];
-#pragma unroll
-            for (int un = 0; un < 4; ++un)
-#pragma unroll
-              for (int t = 0; t < 4; ++t)
-                W[un][t] = scr[((un >> 1) * kRounds * 8 + m * 8 + (un & 1) * 4 + t) * 256];
-            uint32_t rcv[4][2];
-#pragma unroll
-            for (int un = 0; un < 4; ++un)
-#pragma unroll
-              for (int h = 0; h < 2; ++h)
-                rcv[un][h] = __shfl_xor_sync(0xffffffffu, bsel ? W[un][h] : W[un][2 + h], 1);
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int un = 0; un < 4; ++un) {
-                const int a = un >> 1, c = un & 1;
-                const uint32_t own = bsel ? W[un][2 + h] : W[un][h];
-#pragma unroll
+            uint32_t T[2][2][8];  // [h][class][a*4 + b*2 + g]
+            {
+            uint32_t v0[8], v1[8], u0[8], u1[8];
+  #pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              u0[x] = scr[(m * 16 + x) * 256];
+              u1[x] = scr[(m * 16 + 8 + x) * 256];
+              v0[x] = scr[(kRounds * 16 + m * 16 + x) * 256];
+              v1[x] = scr[(kRounds * 16 + m * 16 + 8 + x) * 256];
+            }
+            // This thread holds T_a[b=bsel][g] for k phases t=0..3 (index 2t+g),
+            // a=0 in u, a=1 in v. Thread b owns phases 2b, 2b+1; it sends the
+            // partner (b^1) its values for the partner's phases.
+            uint32_t snd[16], rcv[16];
+  #pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const int h = x >> 1, g = x & 1;
+              const int i_b0 = 2 * (2 + h) + g;  // partner phases when bsel == 0: 2, 3
+              const int i_b1 = 2 * h + g;        // partner phases when bsel == 1: 0, 1
+              snd[x] = bsel ? u0[i_b1] : u0[i_b0];
+              snd[4 + x] = bsel ? u1[i_b1] : u1[i_b0];
+              snd[8 + x] = bsel ? v0[i_b1] : v0[i_b0];
+              snd[12 + x] = bsel ? v1[i_b1] : v1[i_b0];
+            }
+  #pragma unroll
+            for (int x = 0; x < 16; ++x) rcv[x] = __shfl_xor_sync(0xffffffffu, snd[x], 1);
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+  #pragma unroll
+              for (int g = 0; g < 2; ++g) {
+                const int o0 = 2 * h + g, o1 = 2 * (2 + h) + g;  // own index for bsel 0 / 1
+                const uint32_t own_u0 = bsel ? u0[o1] : u0[o0], own_u1 = bsel ? u1[o1] : u1[o0];
+                const uint32_t own_v0 = bsel ? v0[o1] : v0[o0], own_v1 = bsel ? v1[o1] : v1[o0];
+                const int px = h * 2 + g;
+  #pragma unroll
                 for (int bb = 0; bb < 2; ++bb) {
-                  const uint32_t w = (bb == bsel) ? own : rcv[un][h];
-                  T[h][c][a * 4 + bb * 2 + 0] = w & 0xffffu;
-                  T[h][c][a * 4 + bb * 2 + 1] = w >> 16;
+                  const bool mine = bb == bsel;
+                  T[h][0][0 * 4 + bb * 2 + g] = mine ? own_u0 : rcv[px];
+                  T[h][1][0 * 4 + bb * 2 + g] = mine ? own_u1 : rcv[4 + px];
+                  T[h][0][1 * 4 + bb * 2 + g] = mine ? own_v0 : rcv[8 + px];
+                  T[h][1][1 * 4 + bb * 2 + g] = mine ? own_v1 : rcv[12 + px];
                 }
               }
-          } else {
-          uint32_t v0[8], v1[8], u0[8], u1[8];
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            u0[x] = scr[(m * 16 + x) * 256];
-            u1[x] = scr[(m * 16 + 8 + x) * 256];
-            v0[x] = scr[(kRounds * 16 + m * 16 + x) * 256];
-            v1[x] = scr[(kRounds * 16 + m * 16 + 8 + x) * 256];
-          }
-          // This thread holds T_a[b=bsel][g] for k phases t=0..3 (index 2t+g),
-          // a=0 in u, a=1 in v. Thread b owns phases 2b, 2b+1; it sends the
-          // partner (b^1) its values for the partner's phases.
-          uint32_t snd[16], rcv[16];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const int h = x >> 1, g = x & 1;
-            const int i_b0 = 2 * (2 + h) + g;  // partner phases when bsel == 0: 2, 3
-            const int i_b1 = 2 * h + g;        // partner phases when bsel == 1: 0, 1
-            snd[x] = bsel ? u0[i_b1] : u0[i_b0];
-            snd[4 + x] = bsel ? u1[i_b1] : u1[i_b0];
-            snd[8 + x] = bsel ? v0[i_b1] : v0[i_b0];
-            snd[12 + x] = bsel ? v1[i_b1] : v1[i_b0];
-          }
-#pragma unroll
-          for (int x = 0; x < 16; ++x) rcv[x] = __shfl_xor_sync(0xffffffffu, snd[x], 1);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-              const int o0 = 2 * h + g, o1 = 2 * (2 + h) + g;  // own index for bsel 0 / 1
-              const uint32_t own_u0 = bsel ? u0[o1] : u0[o0], own_u1 = bsel ? u1[o1] : u1[o0];
-              const uint32_t own_v0 = bsel ? v0[o1] : v0[o0], own_v1 = bsel ? v1[o1] : v1[o0];
-              const int px = h * 2 + g;
-#pragma unroll
-              for (int bb = 0; bb < 2; ++bb) {
-                const bool mine = bb == bsel;
-                T[h][0][0 * 4 + bb * 2 + g] = mine ? own_u0 : rcv[px];
-                T[h][1][0 * 4 + bb * 2 + g] = mine ? own_u1 : rcv[4 + px];
-                T[h][0][1 * 4 + bb * 2 + g] = mine ? own_v0 : rcv[8 + px];
-                T[h][1][1 * 4 + bb * 2 + g] = mine ? own_v1 : rcv[12 + px];
-              }
             }
-          }
-          }
-          uint32_t kk[2];
-          bool valid[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            kk[h] = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h;
-            valid[h] = j < kk[h] && kk[h] < M && !(s.debug_skip & 1);
-            if (kRanged && valid[h]) {
-              const uint64_t rr = rank_ij + (kk[h] - j - 1);
-              valid[h] = rr >= s.rank_begin && rr < s.rank_end;
             }
-          }
-          uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
-          if (valid[0] || valid[1]) {
-            uint4 pik[2][2];
-            uint2 skc[2][2];
-#pragma unroll
+            uint32_t kk[2];
+            bool valid[2];
+  #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const uint32_t kc = min(kk[h], M - 1);
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                pik[h][c] = __ldg(d.pair[c] + size_t(i) * M + kc);
-                skc[h][c] = __ldg(d.single[c] + kc);
+              kk[h] = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h;
+              valid[h] = j < kk[h] && kk[h] < M && !(s.debug_skip & 1);
+              if (kRanged && valid[h]) {
+                const uint64_t rr = rank_ij + (kk[h] - j - 1);
+                valid[h] = rr >= s.rank_begin && rr < s.rank_end;
               }
-              // slots -> phases 0 and 1; the dropped phase from the pair index
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                const uint32_t P[4] = {pjk[h][c].x, pjk[h][c].y, pjk[h][c].z, pjk[h][c].w};
-                uint32_t* t = T[h][c];
-                if (inf.drop[c] == 1) {
-#pragma unroll
-                  for (int x = 0; x < 4; ++x) t[4 + x] = P[x] - t[x] - t[4 + x];
-                } else if (inf.drop[c] == 0) {
-#pragma unroll
-                  for (int x = 0; x < 4; ++x) {
-                    const uint32_t t1 = t[x];
-                    t[x] = P[x] - t[x] - t[4 + x];
-                    t[4 + x] = t1;
+            }
+            uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
+            if (valid[0] || valid[1]) {
+              uint4 pik[2][2];
+              uint2 skc[2][2];
+  #pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint32_t kc = min(kk[h], M - 1);
+  #pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                  pik[h][c] = __ldg(d.pair[c] + size_t(i) * M + kc);
+                  skc[h][c] = __ldg(d.single[c] + kc);
+                }
+                // slots -> phases 0 and 1; the dropped phase from the pair index
+  #pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                  const uint32_t P[4] = {pjk[h][c].x, pjk[h][c].y, pjk[h][c].z, pjk[h][c].w};
+                  uint32_t* t = T[h][c];
+                  if (inf.drop[c] == 1) {
+  #pragma unroll
+                    for (int x = 0; x < 4; ++x) t[4 + x] = P[x] - t[x] - t[4 + x];
+                  } else if (inf.drop[c] == 0) {
+  #pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                      const uint32_t t1 = t[x];
+                      t[x] = P[x] - t[x] - t[4 + x];
+                      t[4 + x] = t1;
+                    }
                   }
                 }
               }
-            }
-            bool pass[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              uint32_t n0[27], n1[27];
-              derive_cells(T[h][0], pij0, pik[h][0], pjk[h][0], si0, sj0, skc[h][0], d.n[0], n0);
-              derive_cells(T[h][1], pij1, pik[h][1], pjk[h][1], si1, sj1, skc[h][1], d.n[1], n1);
-              if (s.debug_skip & 4)
-                pass[h] = n0[26] == 0x7fffffffu;  // profiling: derivation only
-              else
-                pass[h] = valid[h] && (!s.screen || k2_screen(n0, n1, ktab_s) <= thr_f);
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (pass[h]) {  // rare once the threshold has settled: score exactly
+              bool pass[2];
+  #pragma unroll
+              for (int h = 0; h < 2; ++h) {
                 uint32_t n0[27], n1[27];
                 derive_cells(T[h][0], pij0, pik[h][0], pjk[h][0], si0, sj0, skc[h][0], d.n[0], n0);
                 derive_cells(T[h][1], pij1, pik[h][1], pjk[h][1], si1, sj1, skc[h][1], d.n[1], n1);
-                sk[h] = score_key(k2_device(n0, n1, d.logp));
-                tk[h] = triple_key(i, j, kk[h]);
+                if (s.debug_skip & 4)
+                  pass[h] = n0[26] == 0x7fffffffu;  // profiling: derivation only
+                else
+                  pass[h] = valid[h] && (!s.screen || k2_screen(n0, n1, ktab_s) <= thr_f);
+              }
+  #pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (pass[h]) {  // rare once the threshold has settled: score exactly
+                  uint32_t n0[27], n1[27];
+                  derive_cells(T[h][0], pij0, pik[h][0], pjk[h][0], si0, sj0, skc[h][0], d.n[0], n0);
+                  derive_cells(T[h][1], pij1, pik[h][1], pjk[h][1], si1, sj1, skc[h][1], d.n[1], n1);
+                  sk[h] = score_key(k2_device(n0, n1, d.logp));
+                  tk[h] = triple_key(i, j, kk[h]);
+                }
               }
             }
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const bool want = valid[h] && sk[h] <= gth &&
-                              (nlist < K || key_less(sk[h], tk[h], ls[K - 1], lt[K - 1]));
-            const unsigned cand = __ballot_sync(0xffffffffu, want);
-            if (cand) warp_insert(ls, lt, nlist, K, cand, sk[h], tk[h], lane, s.gthr);
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const bool want = valid[h] && sk[h] <= gth &&
+                                (nlist < K || key_less(sk[h], tk[h], ls[K - 1], lt[K - 1]));
+              const unsigned cand = __ballot_sync(0xffffffffu, want);
+              if (cand) warp_insert(ls, lt, nlist, K, cand, sk[h], tk[h], lane, s.gthr);
+            }
           }
         }
         wk.next(s);
