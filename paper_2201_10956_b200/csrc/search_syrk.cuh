@@ -502,19 +502,36 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           const uint32_t mk1 = (inf.drop[0] == 1 ? 0xffffu : 0u) | (inf.drop[1] == 1 ? 0xffff0000u : 0u);
           const uint32_t mk2 = ~(mk0 | mk1);
           const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
-          for (int m = 0; m < kRounds; ++m) {
-            uint4 pjk[2];
+          // the next round's pair(j,k) entries and scratch words are fetched one
+          // round ahead (software pipelining across rounds)
+          uint4 pjn[2];
+          uint32_t Wn[2][4][2];
+          auto fetch_round = [&](int mm) {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              pjk[h] = __ldg(d.pairp + size_t(min(kbase + 4 * m + h, M - 1)) * M + jc);
-            // W[a][t][g]: this row (j, b=bsel), unit slot a, k phase t, genotype g
-            uint32_t W[2][4][2];
+              pjn[h] = __ldg(d.pairp + size_t(min(kbase + 4 * mm + h, M - 1)) * M + jc);
 #pragma unroll
             for (int a = 0; a < 2; ++a)
 #pragma unroll
               for (int t = 0; t < 4; ++t)
 #pragma unroll
-                for (int g = 0; g < 2; ++g) W[a][t][g] = scr[(a * kRounds * 8 + m * 8 + t * 2 + g) * 256];
+                for (int g = 0; g < 2; ++g)
+                  Wn[a][t][g] = scr[(a * kRounds * 8 + mm * 8 + t * 2 + g) * 256];
+          };
+          fetch_round(0);
+          for (int m = 0; m < kRounds; ++m) {
+            uint4 pjk[2];
+            // W[a][t][g]: this row (j, b=bsel), unit slot a, k phase t, genotype g
+            uint32_t W[2][4][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) pjk[h] = pjn[h];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int g = 0; g < 2; ++g) W[a][t][g] = Wn[a][t][g];
+            if (m + 1 < kRounds) fetch_round(m + 1);
             // the partner row (j, b^1) sends its words for this thread's phases 2*bsel + h
             uint32_t rcv[2][2][2];
 #pragma unroll
