@@ -1113,13 +1113,21 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     CUDA_TRY(dmalloc(ds, &ds->scratch, sizeof(uint32_t) * size_t(grid) *
                                           syrk::kScratchPerThread * 256));
   CUDA_TRY(cudaMemsetAsync(ds->counts[0], 0, sizeof(uint32_t) * grid * tc::kEpilogueWarps, st));
-  size_t tsm = 1024 + size_t(syrk::kSStages) * syrk::kSStageBytes +
-               size_t(tc::kEpilogueWarps) * 2 * K * sizeof(uint64_t);
-  // the K2 screen needs its table in shared memory; without room, every
-  // valid triple is scored exactly from the global fp64 table
-  const bool screen = tsm + sizeof(float) * ds->ktab_n <= ds->smem_optin - 2048 &&
-                      !std::getenv("E3_NO_SCREEN");
-  if (screen) tsm += sizeof(float) * ds->ktab_n;
+  // Shared memory: operand stages + top-k lists + (optionally) the K2 screening
+  // table. The screen pays for itself many times over, so when the table does
+  // not fit beside four stages the kernel runs with fewer (>= 2).
+  const size_t lists_b = size_t(tc::kEpilogueWarps) * 2 * K * sizeof(uint64_t);
+  const size_t tab_b = sizeof(float) * ds->ktab_n;
+  const size_t cap = ds->smem_optin - 2048;
+  uint32_t nst = syrk::kSStages;
+  bool screen = !std::getenv("E3_NO_SCREEN");
+  if (const char* e = std::getenv("E3_SYRK_STAGES")) nst = uint32_t(std::max(2, std::min(syrk::kSStages, std::atoi(e))));
+  if (screen) {
+    while (nst > 2 && 1024 + nst * syrk::kSStageBytes + lists_b + tab_b > cap) --nst;
+    screen = 1024 + nst * syrk::kSStageBytes + lists_b + tab_b <= cap;
+    if (!screen) nst = syrk::kSStages;
+  }
+  const size_t tsm = 1024 + nst * syrk::kSStageBytes + lists_b + (screen ? tab_b : 0);
   // compaction waits for the metadata upload (and all earlier work on st)
   CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_upload, 0));
   for (size_t b = 0; b < batches.size(); ++b) {
@@ -1144,6 +1152,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.scratch = ds->scratch;
     sa.debug_skip = ds->debug_skip;
     sa.screen = screen ? 1u : 0u;
+    sa.nst = nst;
     // batch b's compaction overlaps batch b-1's search; it may reuse buffer
     // b & 1 only once batch b-2's search is done with it
     if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_sdone[buf], 0));

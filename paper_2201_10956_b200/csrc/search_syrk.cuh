@@ -33,7 +33,7 @@ constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows ea
 constexpr int kSChunk = 256;                           // samples per stage
 constexpr int kSRowBytes = kSChunk / 2;                // 128 B per operand row
 constexpr int kSStageBytes = 2 * kRows * kSRowBytes;   // A + B = 32 KiB
-constexpr int kSStages = 4;
+constexpr int kSStages = 4;   // stage slots compiled in; a launch uses s.nst of them
 constexpr int kUnits = 3;          // TMEM ring of (tile, a, c) accumulators, 128 columns each
 constexpr uint32_t kSfCol = 384;   // scale-factor columns (UE8M0 1.0)
 constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10)          // A, B = E2M1
@@ -116,6 +116,7 @@ struct SyrkArgs {
   uint32_t* scratch;                 // [grid][kRounds * 16][256]
   uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no K2, 2 = no expansion
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
+  uint32_t nst;                      // operand stages in use (2..kSStages)
 };
 
 // S_{i,a,c}: block-wide exclusive scan of popcounts over the class words of X_a^i.
@@ -261,7 +262,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* stages = smem;
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + kSStages * kSStageBytes);
+  const uint32_t nst = s.nst;  // operand stages in use (fewer frees room for the K2 table)
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + nst * kSStageBytes);
   float* ktab = reinterpret_cast<float*>(lists + size_t(kEpilogueWarps) * 2 * s.top_k);
   __shared__ uint64_t full_bar[kSStages], empty_bar[kSStages];
   __shared__ uint64_t tfull_bar[kUnits], tempty_bar[kUnits];
@@ -335,8 +337,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             const uint32_t nch = inf.q[a][c] / 2;
             const uint32_t dcol = tmem + slot * 128;
             for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
-              const uint32_t st = n % kSStages;
-              mbar_wait_spin(&full_bar[st], (n / kSStages) & 1);
+              const uint32_t st = n % nst;
+              mbar_wait_spin(&full_bar[st], (n / nst) & 1);
               fence_after();
               const uint32_t abase = smem_u32(stages + st * kSStageBytes);
               const uint32_t bbase = abase + kRows * kSRowBytes;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&full_bar[st]);
-            if (++st == kSStages) { st = 0; ph ^= 1; }
+            if (++st == nst) { st = 0; ph ^= 1; }
           }
         }
         wk.next(s);
