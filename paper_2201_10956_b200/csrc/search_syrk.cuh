@@ -444,8 +444,37 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         const IInfo inf = s.info[wk.ii];
         const uint32_t i = s.i_lo + wk.ii;
         // ---- drain the four units (a, c) of this tile: TMEM (f32 counts) ->
-        // u32 scratch, releasing each ring slot at once so the MMAs of the
-        // next units overlap the scoring below.
+        // scratch, releasing each ring slot as soon as it is copied, so the MMAs
+        // of the next units overlap the scoring below.
+        if constexpr (kNarrow) {
+          // the two classes of slot a are drained together into class-packed
+          // words (a, m, t, g) = class0 | class1 << 16
+#pragma unroll
+          for (uint32_t a = 0; a < 2; ++a, u += 2) {
+            const uint32_t s0 = u % kUnits, s1 = (u + 1) % kUnits;
+            mbar_wait_sleep(&tfull_bar[s0], (u / kUnits) & 1);
+            mbar_wait_sleep(&tfull_bar[s1], ((u + 1) / kUnits) & 1);
+            fence_after();
+            const uint32_t keep0 = inf.q[a][0] ? 0xffffffffu : 0u, keep1 = inf.q[a][1] ? 0xffffffffu : 0u;
+            const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + half * 8 * kRounds;
+#pragma unroll
+            for (int m2 = 0; m2 < kRounds; m2 += 2) {
+              uint32_t v0[16], v1[16];
+              tmem_ld16(tbase + s0 * 128 + 8 * m2, v0);
+              tmem_ld16(tbase + s1 * 128 + 8 * m2, v1);
+              tmem_wait_ld();
+#pragma unroll
+              for (int x = 0; x < 16; ++x) {
+                const int m = m2 + (x >> 3), tg = x & 7;
+                scr[(a * kRounds * 8 + m * 8 + tg) * 256] =
+                    (f32_count(v0[x]) & keep0) | ((f32_count(v1[x]) & keep1) << 16);
+              }
+            }
+            fence_before();
+            mbar_arrive(&tempty_bar[s0]);
+            mbar_arrive(&tempty_bar[s1]);
+          }
+        } else {
 #pragma unroll
         for (uint32_t a = 0; a < 2; ++a)
 #pragma unroll
@@ -461,27 +490,17 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               uint32_t v[16];
               tmem_ld16(taddr + 8 * m2, v);
               tmem_wait_ld();
-              if constexpr (kNarrow) {
-                // u16 half c of word (a, m, t, g)
-                uint16_t* scr16 = reinterpret_cast<uint16_t*>(scr);
 #pragma unroll
-                for (int x = 0; x < 16; ++x) {
-                  const int m = m2 + (x >> 3), tg = x & 7;
-                  scr16[(a * kRounds * 8 + m * 8 + tg) * 512 + c] =
-                      nonempty ? uint16_t(f32_count(v[x])) : uint16_t(0);
-                }
-              } else {
-#pragma unroll
-                for (int x = 0; x < 16; ++x) {
-                  const int m = m2 + (x >> 3);
-                  scr[(a * kRounds * 16 + m * 16 + c * 8 + (x & 7)) * 256] =
-                      nonempty ? f32_count(v[x]) : 0u;
-                }
+              for (int x = 0; x < 16; ++x) {
+                const int m = m2 + (x >> 3);
+                scr[(a * kRounds * 16 + m * 16 + c * 8 + (x & 7)) * 256] =
+                    nonempty ? f32_count(v[x]) : 0u;
               }
             }
             fence_before();
             mbar_arrive(&tempty_bar[slot]);
           }
+        }
         const uint32_t j = i + 1 + wk.jb * kJB + jl;
         const uint32_t jc = min(j, M - 1);
         const uint64_t gth = *reinterpret_cast<volatile uint64_t*>(s.gthr);
