@@ -452,8 +452,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
           for (uint32_t a = 0; a < 2; ++a, u += 2) {
             const uint32_t s0 = u % kUnits, s1 = (u + 1) % kUnits;
-            mbar_wait_sleep(&tfull_bar[s0], (u / kUnits) & 1);
-            mbar_wait_sleep(&tfull_bar[s1], ((u + 1) / kUnits) & 1);
+            mbar_wait(&tfull_bar[s0], (u / kUnits) & 1);
+            mbar_wait(&tfull_bar[s1], ((u + 1) / kUnits) & 1);
             fence_after();
             const uint32_t keep0 = inf.q[a][0] ? 0xffffffffu : 0u, keep1 = inf.q[a][1] ? 0xffffffffu : 0u;
             const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + half * 8 * kRounds;
