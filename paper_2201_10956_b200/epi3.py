@@ -409,7 +409,8 @@ class DeviceDataset:
         return self._h
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
+        # at interpreter exit the module global `lib` may already be gone
+        if getattr(self, "_h", None) and lib is not None:
             lib.e3_dataset_destroy(self._h)
             self._h = None
 
