@@ -37,6 +37,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -530,15 +532,21 @@ __global__ void repack_kernel(const uint64_t* __restrict__ raw, uint32_t M, uint
 
 __global__ void singles_kernel(const uint4* __restrict__ planes, uint32_t M, uint32_t wq,
                                uint2* __restrict__ single) {
-  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per SNP: lanes stride over the word-quads, then a shuffle sum
+  const uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (x >= M) return;
   uint32_t s0 = 0, s1 = 0;
-  for (uint32_t w = 0; w < wq; ++w) {
+  for (uint32_t w = lane; w < wq; w += 32) {
     const uint4 a = planes[(size_t(w) * M + x) * 2], b = planes[(size_t(w) * M + x) * 2 + 1];
     s0 += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
     s1 += __popc(b.x) + __popc(b.y) + __popc(b.z) + __popc(b.w);
   }
-  single[x] = make_uint2(s0, s1);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if (lane == 0) single[x] = make_uint2(s0, s1);
 }
 
 // pair[x*M + y] for x < y: {popc(X0x&X0y), popc(X0x&X1y), popc(X1x&X0y), popc(X1x&X1y)}.
@@ -752,6 +760,44 @@ double k2_screen_margin(double gmax, double N, double alpha) {
   return 2.0 * 27.0 * per_cell + 1e-9 * smax + 1e-6;
 }
 
+// Host tables that depend only on N: the reference's log table (built exactly
+// like build_log_table(N+1), scoring.cpp:14-21) and the K2 screening table
+// G[n] = fl32(P[n] - alpha*n) with its proven margin. alpha balances the
+// extremes of P[n] - alpha*n over [0, N+1] (about -0.28 N .. +0.28 N), which
+// keeps the fp32 rounding small; the affine part cancels per cell up to alpha.
+// The tables are immutable, so dataset creations with the same N share them
+// (a small per-process cache; the e2e path recreates datasets per step).
+struct LogTables {
+  std::vector<double> logp;  // N+2 entries
+  std::vector<float> ktab;   // N+2 rounded up to a multiple of 4
+  double kshift = 0;
+};
+std::shared_ptr<const LogTables> log_tables_for(uint64_t N) {
+  static std::mutex mu;
+  static std::vector<std::pair<uint64_t, std::shared_ptr<const LogTables>>> cache;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (const auto& e : cache)
+      if (e.first == N) return e.second;
+  }
+  auto t = std::make_shared<LogTables>();
+  t->logp.resize(N + 2);
+  e3_build_log_table(N + 1, t->logp.data());
+  const double alpha = std::log(double(N) + 1.0) - 1.2785;
+  t->ktab.assign((N + 2 + 3) / 4 * 4, 0.f);
+  double gmax = 0;
+  for (uint64_t n = 0; n < N + 2; ++n) {
+    const double g = t->logp[n] - alpha * double(n);
+    t->ktab[n] = float(g);
+    gmax = std::max(gmax, std::fabs(g));
+  }
+  t->kshift = -27.0 * alpha + k2_screen_margin(gmax, double(N), alpha);
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() >= 4) cache.erase(cache.begin());
+  cache.emplace_back(N, t);
+  return t;
+}
+
 int build(e3_dataset* ds, const uint64_t* host[2]) {
   // E3_TRACE_CREATE=1: per-phase wall times of dataset creation on stderr
   const bool trace = std::getenv("E3_TRACE_CREATE") != nullptr;
@@ -815,8 +861,8 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     const uint64_t threads = uint64_t(ds->wq[c]) * M;
     repack_kernel<<<unsigned((threads + 255) / 256), 256, 0, ds->stream>>>(
         raw, M, w64, ds->wq[c], tail, ds->planes[c], bad);
-    singles_kernel<<<(M + 255) / 256, 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
-                                                          ds->single[c]);
+    singles_kernel<<<(M + 7) / 8, 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
+                                                      ds->single[c]);
     CUDA_TRY(cudaGetLastError());
     dfree(ds, raw);
   }
@@ -865,28 +911,17 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     CUDA_TRY(cudaMemcpyAsync(ds->h_single[c].data(), ds->single[c], sizeof(uint2) * M,
                              cudaMemcpyDeviceToHost, ds->stream));
   }
-  // K2 log table, built on the host exactly like build_log_table(N+1).
+  // K2 log table (exactly build_log_table(N+1)) and screening table: pure
+  // functions of N, built once per N per process (log_tables_for).
   const uint64_t N = ds->N[0] + ds->N[1];
-  std::vector<double> logp(N + 2);
-  e3_build_log_table(N + 1, logp.data());
-  CUDA_TRY(dmalloc(ds, &ds->logp, sizeof(double) * logp.size()));
-  CUDA_TRY(cudaMemcpyAsync(ds->logp, logp.data(), sizeof(double) * logp.size(),
+  const std::shared_ptr<const LogTables> lt = log_tables_for(N);
+  CUDA_TRY(dmalloc(ds, &ds->logp, sizeof(double) * lt->logp.size()));
+  CUDA_TRY(cudaMemcpyAsync(ds->logp, lt->logp.data(), sizeof(double) * lt->logp.size(),
                            cudaMemcpyHostToDevice, ds->stream));
-  // K2 screening table G[n] = fl32(P[n] - alpha*n): alpha balances the extremes
-  // of P[n] - alpha*n over [0, N+1] (about -0.28 N .. +0.28 N), which keeps the
-  // fp32 rounding small; the affine part cancels per cell up to alpha.
-  const double alpha = std::log(double(N) + 1.0) - 1.2785;
-  ds->ktab_n = uint32_t((N + 2 + 3) / 4 * 4);
-  std::vector<float> ktab(ds->ktab_n, 0.f);
-  double gmax = 0;
-  for (uint64_t n = 0; n < N + 2; ++n) {
-    const double g = logp[n] - alpha * double(n);
-    ktab[n] = float(g);
-    gmax = std::max(gmax, std::fabs(g));
-  }
-  ds->kshift = -27.0 * alpha + k2_screen_margin(gmax, double(N), alpha);
-  CUDA_TRY(dmalloc(ds, &ds->ktab, sizeof(float) * ktab.size()));
-  CUDA_TRY(cudaMemcpyAsync(ds->ktab, ktab.data(), sizeof(float) * ktab.size(),
+  ds->ktab_n = uint32_t(lt->ktab.size());
+  ds->kshift = lt->kshift;
+  CUDA_TRY(dmalloc(ds, &ds->ktab, sizeof(float) * lt->ktab.size()));
+  CUDA_TRY(cudaMemcpyAsync(ds->ktab, lt->ktab.data(), sizeof(float) * lt->ktab.size(),
                            cudaMemcpyHostToDevice, ds->stream));
   // Item prefix over i (items = 32x32 (j,k) tiles above i, i-major).
   ds->h_itemoff.assign(M - 1, 0);
