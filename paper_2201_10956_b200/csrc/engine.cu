@@ -878,7 +878,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     pairs_tc::PArgs pa{};
     pa.M = M;
     pa.nb = (M + pairs_tc::kBlk - 1) / pairs_tc::kBlk;
-    pa.units = 2ull * pa.nb * (pa.nb + 1) / 2;
+    pa.tiles = uint64_t(pa.nb) * (pa.nb + 1) / 2;
     pa.pairp = ds->pairp;
     for (int c = 0; c < 2; ++c) {
       pa.wq[c] = ds->wq[c];
@@ -892,7 +892,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(pairs_tc::smem_bytes())));
-    const uint32_t grid = uint32_t(std::min<uint64_t>(ds->num_sms, pa.units));
+    const uint32_t grid = uint32_t(std::min<uint64_t>(ds->num_sms, pa.tiles));
     if (std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 23)) {
       if (ds->narrow)
         pairs_tc::pairs_tc_kernel<true><<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);

@@ -9,9 +9,10 @@
 // E2M1 0/1 nibbles (exact: counts < 2^23). Replaces the POPC pairs_kernel
 // (15.6 ms at 8192 x 16384) in dataset creation.
 //
-// Warp roles: warp 0 issues the MMAs, warps 1-4 expand plane quads into the
-// fp4 stages (thread r owns A row r and B row r), warps 5-8 drain TMEM and
-// write both triangles of the index.
+// Warp roles: warp 0 issues the MMAs (per tile: class 0 then class 1 into a
+// 3-slot TMEM ring), warps 1-4 expand plane quads into the fp4 stages (thread
+// r owns A row r and B row r), warps 5-8 drain both classes of a tile
+// together and write the index (class-packed in narrow mode).
 
 namespace pairs_tc {
 
@@ -32,49 +33,48 @@ struct PArgs {
   const uint4* planes[2];   // [wq + 1][M][2]
   uint4* pair[2];           // [M * M] wide (u32) counts
   uint4* pairp;             // [M * M] narrow class-packed mirror (c0 | c1 << 16), every N_c < 2^16
-  uint64_t units;           // 2 classes x nb (nb + 1) / 2 tiles
+  uint64_t tiles;           // nb (nb + 1) / 2 tiles; each = two units (class 0, class 1)
 };
 
-// unit -> (class, x-block, y-block), class-major, row-major triangle xb <= yb
+// tile -> (x-block, y-block), row-major triangle xb <= yb
 struct PWalker {
-  uint32_t c, xb, yb, nb;
-  __device__ void start(const PArgs& p, uint64_t u) {
+  uint32_t xb, yb, nb;
+  __device__ void start(const PArgs& p, uint64_t t) {
     nb = p.nb;
-    const uint64_t per = uint64_t(nb) * (nb + 1) / 2;
-    c = uint32_t(u / per);
-    uint64_t r = u % per;
     xb = 0;
-    while (r >= uint64_t(nb - xb)) { r -= nb - xb; ++xb; }
-    yb = xb + uint32_t(r);
+    while (t >= uint64_t(nb - xb)) { t -= nb - xb; ++xb; }
+    yb = xb + uint32_t(t);
   }
   __device__ void next() {
     if (++yb == nb) {
-      if (++xb == nb) { xb = 0; ++c; }
+      ++xb;
       yb = xb;
     }
   }
 };
 
+constexpr int kRing = 3;  // TMEM accumulators (128 columns each) + scale factors at kSfCol
+
 // kNarrow: the wide index gets the upper triangle only (what the other
-// engines read) and the SYRK engine's mirrored index is written narrow.
+// engines read) and the SYRK engine's mirrored index is written class-packed.
 template <bool kNarrow>
 __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
   __shared__ uint64_t full_bar[kStagesP], empty_bar[kStagesP];
-  __shared__ uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint64_t tfull_bar[kRing], tempty_bar[kRing];
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t u0 = p.units * blockIdx.x / gridDim.x;
-  const uint64_t u1 = p.units * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t t0 = p.tiles * blockIdx.x / gridDim.x;
+  const uint64_t t1 = p.tiles * (blockIdx.x + 1) / gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStagesP; ++st) {
       mbar_init(&full_bar[st], kProd);
       mbar_init(&empty_bar[st], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kRing; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 32 * kDrain);
     }
@@ -104,31 +104,31 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
   fence_after();
 
   if (warp == 0) {
-    if (lane == 0 && u0 < u1) {
-      PWalker wk;
-      wk.start(p, u0);
-      uint32_t n = 0;
+    if (lane == 0 && t0 < t1) {
+      uint32_t n = 0, u = 0;
       const uint32_t tsf = tmem + kSfCol;
-      for (uint64_t u = u0; u < u1; ++u) {
-        const uint32_t t = uint32_t(u - u0), slot = t & 1;
-        mbar_wait(&tempty_bar[slot], ((t >> 1) & 1) ^ 1);
-        fence_after();
-        const uint32_t nch = (p.wq[wk.c] + 1) / 2;
-        const uint32_t dcol = tmem + slot * 128;
-        for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
-          const uint32_t st = n % kStagesP;
-          mbar_wait_spin(&full_bar[st], (n / kStagesP) & 1);
-          fence_after();
-          const uint32_t abase = smem_u32(stages + st * kSStageBytes);
-          const uint32_t bbase = abase + kRows * kSRowBytes;
+      for (uint64_t t = t0; t < t1; ++t) {
 #pragma unroll
-          for (int kk = 0; kk < kSRowBytes / 32; ++kk)
-            syrk::mma_f4(dcol, syrk::f4_desc(abase + kk * 256), syrk::f4_desc(bbase + kk * 256), tsf,
-                         (ch != 0 || kk != 0) ? 1u : 0u);
-          mma_commit(&empty_bar[st]);
+        for (uint32_t c = 0; c < 2; ++c, ++u) {
+          const uint32_t slot = u % kRing;
+          mbar_wait(&tempty_bar[slot], ((u / kRing) & 1) ^ 1);
+          fence_after();
+          const uint32_t nch = (p.wq[c] + 1) / 2;
+          const uint32_t dcol = tmem + slot * 128;
+          for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
+            const uint32_t st = n % kStagesP;
+            mbar_wait_spin(&full_bar[st], (n / kStagesP) & 1);
+            fence_after();
+            const uint32_t abase = smem_u32(stages + st * kSStageBytes);
+            const uint32_t bbase = abase + kRows * kSRowBytes;
+#pragma unroll
+            for (int kk = 0; kk < kSRowBytes / 32; ++kk)
+              syrk::mma_f4(dcol, syrk::f4_desc(abase + kk * 256), syrk::f4_desc(bbase + kk * 256), tsf,
+                           (ch != 0 || kk != 0) ? 1u : 0u);
+            mma_commit(&empty_bar[st]);
+          }
+          mma_commit(&tfull_bar[slot]);
         }
-        mma_commit(&tfull_bar[slot]);
-        wk.next();
       }
     }
     __syncwarp();
@@ -136,88 +136,97 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
     const int r = threadIdx.x - 32;  // 0..127
     const uint32_t row_off = (r >> 3) * (kSRowBytes / 16) * 128 + (r & 7) * 16;
     const uint32_t stage_a = smem_u32(stages) + row_off, stage_b = stage_a + kRows * kSRowBytes;
-    if (u0 < u1) {
+    if (t0 < t1) {
       PWalker wk;
-      wk.start(p, u0);
+      wk.start(p, t0);
       uint32_t st = 0, ph = 0;
       const uint32_t rmax = 2 * p.M - 1;
-      for (uint64_t u = u0; u < u1; ++u) {
-        const size_t row = size_t(p.M) * 2;
-        const uint4* pl = p.planes[wk.c];
-        const uint4* Ya = pl + min(2 * kBlk * wk.xb + r, rmax);
-        const uint4* Yb = pl + min(2 * kBlk * wk.yb + r, rmax);
-        const uint32_t nq = (p.wq[wk.c] + 1) / 2 * 2;  // zero quad pads an odd count
-        uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
-        if (nq) {
-          a0 = __ldg(Ya); a1 = __ldg(Ya + row);
-          b0 = __ldg(Yb); b1 = __ldg(Yb + row);
-        }
-        for (uint32_t q = 0; q < nq; q += 2) {
-          const uint4 ca0 = a0, ca1 = a1, cb0 = b0, cb1 = b1;
-          if (q + 2 < nq) {
-            const size_t o = size_t(q + 2) * row;
-            a0 = __ldg(Ya + o); a1 = __ldg(Ya + o + row);
-            b0 = __ldg(Yb + o); b1 = __ldg(Yb + o + row);
+      const size_t row = size_t(p.M) * 2;
+      for (uint64_t t = t0; t < t1; ++t) {
+#pragma unroll 1
+        for (uint32_t c = 0; c < 2; ++c) {
+          const uint4* pl = p.planes[c];
+          const uint4* Ya = pl + min(2 * kBlk * wk.xb + r, rmax);
+          const uint4* Yb = pl + min(2 * kBlk * wk.yb + r, rmax);
+          const uint32_t nq = (p.wq[c] + 1) / 2 * 2;  // zero quad pads an odd count
+          uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
+          if (nq) {
+            a0 = __ldg(Ya); a1 = __ldg(Ya + row);
+            b0 = __ldg(Yb); b1 = __ldg(Yb + row);
           }
-          mbar_wait(&empty_bar[st], ph ^ 1);
-          const uint32_t so = st * kSStageBytes;
-          syrk::expand_quad_f4(stage_a + so, 0, ca0);
-          syrk::expand_quad_f4(stage_a + so, 1, ca1);
-          syrk::expand_quad_f4(stage_b + so, 0, cb0);
-          syrk::expand_quad_f4(stage_b + so, 1, cb1);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full_bar[st]);
-          if (++st == kStagesP) { st = 0; ph ^= 1; }
+          for (uint32_t q = 0; q < nq; q += 2) {
+            const uint4 ca0 = a0, ca1 = a1, cb0 = b0, cb1 = b1;
+            if (q + 2 < nq) {
+              const size_t o = size_t(q + 2) * row;
+              a0 = __ldg(Ya + o); a1 = __ldg(Ya + o + row);
+              b0 = __ldg(Yb + o); b1 = __ldg(Yb + o + row);
+            }
+            mbar_wait(&empty_bar[st], ph ^ 1);
+            const uint32_t so = st * kSStageBytes;
+            syrk::expand_quad_f4(stage_a + so, 0, ca0);
+            syrk::expand_quad_f4(stage_a + so, 1, ca1);
+            syrk::expand_quad_f4(stage_b + so, 0, cb0);
+            syrk::expand_quad_f4(stage_b + so, 1, cb1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full_bar[st]);
+            if (++st == kStagesP) { st = 0; ph ^= 1; }
+          }
         }
         wk.next();
       }
     }
   } else {
-    // drain: lane = row (x, a); columns (y, b) -> uint2 {b=0, b=1} at
-    // component offset 2a of pair[x*M + y] and of the mirror pair[y*M + x]
+    // drain both classes of a tile together: lane = row (x, a), columns (y, b)
+    // -> wide uint2 {b=0, b=1} at component offset 2a of pair[c][x*M + y]
+    // (and its mirror unless narrow), narrow class-packed uint2 at offset 2a of
+    // pairp[x*M + y] and pairp[y*M + x]
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const int a = row & 1;
-    if (u0 < u1) {
+    if (t0 < t1) {
       PWalker wk;
-      wk.start(p, u0);
-      for (uint64_t u = u0; u < u1; ++u) {
-        const uint32_t t = uint32_t(u - u0), slot = t & 1;
-        mbar_wait_sleep(&tfull_bar[slot], (t >> 1) & 1);
+      wk.start(p, t0);
+      uint32_t u = 0;
+      const bool e0 = p.wq[0] == 0, e1 = p.wq[1] == 0;
+      for (uint64_t t = t0; t < t1; ++t, u += 2) {
+        const uint32_t s0 = u % kRing, s1 = (u + 1) % kRing;
+        mbar_wait(&tfull_bar[s0], (u / kRing) & 1);
+        mbar_wait(&tfull_bar[s1], ((u + 1) / kRing) & 1);
         fence_after();
         const uint32_t x = wk.xb * kBlk + (row >> 1);
-        const bool empty = p.wq[wk.c] == 0;
-        uint32_t* base = reinterpret_cast<uint32_t*>(p.pair[wk.c]);
-        const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + slot * 128;
+        const uint32_t tb = tmem + (uint32_t(quarter * 32) << 16);
 #pragma unroll 1
         for (int c16 = 0; c16 < 128; c16 += 16) {
-          uint32_t v[16];
-          syrk::tmem_ld16(taddr + c16, v);
+          uint32_t v0[16], v1[16];
+          syrk::tmem_ld16(tb + s0 * 128 + c16, v0);
+          syrk::tmem_ld16(tb + s1 * 128 + c16, v1);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const uint32_t y = wk.yb * kBlk + (c16 >> 1) + e;
             if (x < y && y < p.M) {
-              const uint2 w = empty ? make_uint2(0u, 0u)
-                                    : make_uint2(syrk::f32_count(v[2 * e]), syrk::f32_count(v[2 * e + 1]));
-              *reinterpret_cast<uint2*>(base + (size_t(x) * p.M + y) * 4 + 2 * a) = w;
-              if (kNarrow) {  // u16 halves: class c of components (a, b=0), (a, b=1)
-                uint16_t* nb = reinterpret_cast<uint16_t*>(p.pairp);
-                const size_t o1 = (size_t(x) * p.M + y) * 8 + a * 4 + wk.c;
-                const size_t o2 = (size_t(y) * p.M + x) * 8 + a * 4 + wk.c;
-                nb[o1] = uint16_t(w.x);
-                nb[o1 + 2] = uint16_t(w.y);
-                nb[o2] = uint16_t(w.x);
-                nb[o2 + 2] = uint16_t(w.y);
+              const uint2 w0 = e0 ? make_uint2(0u, 0u)
+                                  : make_uint2(syrk::f32_count(v0[2 * e]), syrk::f32_count(v0[2 * e + 1]));
+              const uint2 w1 = e1 ? make_uint2(0u, 0u)
+                                  : make_uint2(syrk::f32_count(v1[2 * e]), syrk::f32_count(v1[2 * e + 1]));
+              const size_t up = size_t(x) * p.M + y, lo = size_t(y) * p.M + x;
+              *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[0] + up) + 2 * a) = w0;
+              *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[1] + up) + 2 * a) = w1;
+              if (kNarrow) {
+                const uint2 pk = make_uint2(w0.x | (w1.x << 16), w0.y | (w1.y << 16));
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pairp + up) + 2 * a) = pk;
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pairp + lo) + 2 * a) = pk;
               } else {
-                *reinterpret_cast<uint2*>(base + (size_t(y) * p.M + x) * 4 + 2 * a) = w;
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[0] + lo) + 2 * a) = w0;
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[1] + lo) + 2 * a) = w1;
               }
             }
           }
         }
         fence_before();
-        mbar_arrive(&tempty_bar[slot]);
+        mbar_arrive(&tempty_bar[s0]);
+        mbar_arrive(&tempty_bar[s1]);
         wk.next();
       }
     }
