@@ -1059,6 +1059,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     return c3(M) - c3(M - i);
   };
   constexpr size_t kYBudget = size_t(3) << 20;   // uint4 elements per batch (48 MiB)
+  constexpr size_t kYMax = size_t(16) << 20;     // hard cap (256 MiB per buffer)
   struct Batch {
     uint32_t first, n, rmax, qmax;
     size_t ytot, ptot;
@@ -1093,7 +1094,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
           ++p;
         }
       }
-      if (bt.n > 0 && bt.ytot + ysz > kYBudget) break;
+      // a batch closes at the L2-sized budget once it has enough tiles to
+      // keep every SM busy; batches of few tiles (long sample axis, cfg4)
+      // may grow up to kYMax
+      const uint64_t bt_tiles = offs.back();
+      if (bt.n > 0 && bt.ytot + ysz > kYBudget &&
+          (bt_tiles >= 2ull * grid || bt.ytot + ysz > kYMax))
+        break;
       for (int a = 0; a < 2; ++a) {
         inf.y_off[a] = bt.ytot;
         bt.ytot += size_t(inf.q[a][0] + inf.q[a][1]) * inf.R;
