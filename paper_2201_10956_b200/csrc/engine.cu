@@ -648,6 +648,7 @@ struct e3_dataset {
   size_t smem_optin = 0;
   uint32_t debug_skip = 0;  // E3_DEBUG_SKIP (profiling experiments only)
   bool no_drop = false;     // E3_SYRK_NO_DROP: always compute phases 0 and 1 (A/B testing)
+  bool old_compact = false; // E3_OLD_COMPACT: always positions + gather kernels (A/B testing)
   // scratch reused across searches
   ulonglong2* lists[2] = {nullptr, nullptr};
   uint32_t* counts[2] = {nullptr, nullptr};
@@ -949,6 +950,7 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   ds->smem_optin = size_t(smem_optin);
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
+  ds->old_compact = std::getenv("E3_OLD_COMPACT") != nullptr;
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
@@ -1198,10 +1200,19 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     // batch b's compaction overlaps batch b-1's search; it may reuse buffer
     // b & 1 only once batch b-2's search is done with it
     if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_sdone[buf], 0));
-    syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, ds->cstream>>>(d, sa, pbuf);
-    if (bt.qmax > 0)
-      syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0,
-                                    ds->cstream>>>(d, sa, pbuf, ybuf);
+    // bit-compress kernel: one block walks a class's whole sample axis, which
+    // pays off while that axis is short; long axes use positions + gather,
+    // which parallelise over output quads
+    const bool pext = !ds->old_compact && std::max(ds->N[0], ds->N[1]) <= 16384;
+    if (!pext) {
+      syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, ds->cstream>>>(d, sa, pbuf);
+      if (bt.qmax > 0)
+        syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0,
+                                      ds->cstream>>>(d, sa, pbuf, ybuf);
+    } else {
+      syrk::compact_pext_kernel<<<dim3((bt.rmax + 127) / 128, 4, bt.n), 128, 0, ds->cstream>>>(
+          d, sa, ybuf);
+    }
     CUDA_TRY(cudaEventRecord(ds->ev_cdone[buf], ds->cstream));
     CUDA_TRY(cudaStreamWaitEvent(st, ds->ev_cdone[buf], 0));
     // only batches holding a partially covered first SNP need per-triple rank

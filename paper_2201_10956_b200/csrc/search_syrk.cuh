@@ -223,6 +223,107 @@ __global__ void __launch_bounds__(128) compact_gather_kernel(const DevData d, Sy
   Y[inf.y_off[a] + size_t(q) * inf.R + row] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
 }
 
+// Y_{i,p} by bit compression: for slot p (phase a) and class c, every
+// operand row (j, b) keeps the bits of X_b^j at the samples where SNP i has
+// genotype a, in sample order (= positions ascending). The mask word of i is
+// shared by all rows of the block, so the five shift masks of the parallel
+// compress (Hacker's Delight 7-4) are computed once per word into shared
+// memory; each row then compresses a source word in 16 ALU ops and appends
+// popc(mask) bits to a 64-bit accumulator that emits 128-bit output quads.
+// Block = 128 rows of one (i, p, c); rows read/write coalesced uint4s.
+__global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, const SyrkArgs s,
+                                                           uint4* __restrict__ Y) {
+  const uint32_t ii = blockIdx.z, p = blockIdx.y >> 1, c = blockIdx.y & 1;
+  const IInfo* inf = s.info + ii;
+  const uint32_t i = s.i_lo + ii;
+  const uint32_t R = inf->R;
+  if (blockIdx.x * 128 >= R) return;
+  const uint32_t drop = inf->drop[c];
+  const uint32_t a = (p == 0) ? (drop == 0 ? 1u : 0u) : (drop == 2 ? 1u : 2u);
+  const uint32_t qout = inf->q[p][c];
+  const uint32_t row = blockIdx.x * 128 + threadIdx.x;
+  const bool active = row < R;
+  const uint32_t snp = min(i + 1 + (row >> 1), d.M - 1), g = row & 1;
+  const uint32_t ncls = d.n[c];
+  const uint32_t nw = (ncls + 31) / 32;  // source words of the class
+  const size_t rstride = size_t(d.M) * 2;
+  const uint4* pl = c ? d.planes[1] : d.planes[0];
+  uint4* dst = Y + inf->y_off[p] + size_t(c ? inf->q[p][0] : 0) * R + row;
+  __shared__ uint32_t smv[5][128], smask[128];
+  uint64_t acc = 0;
+  uint32_t nacc = 0, nq = 0, ne = 0;
+  uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+  auto emit = [&](uint32_t w) {  // uniform across the block: counts depend on the mask only
+    o0 = o1; o1 = o2; o2 = o3; o3 = w;
+    if (++ne == 4) {
+      if (active) dst[size_t(nq) * R] = make_uint4(o0, o1, o2, o3);
+      ++nq;
+      ne = 0;
+    }
+  };
+  for (uint32_t w0 = 0; w0 < nw; w0 += 128) {
+    {
+      const uint32_t w = w0 + threadIdx.x;
+      uint32_t m = 0;
+      if (w < nw) {
+        const uint4 q0 = __ldg(pl + size_t(w >> 2) * rstride + 2 * i);
+        const uint4 q1 = __ldg(pl + size_t(w >> 2) * rstride + 2 * i + 1);
+        const uint32_t c0[4] = {q0.x, q0.y, q0.z, q0.w}, c1[4] = {q1.x, q1.y, q1.z, q1.w};
+        if (a == 0) m = c0[w & 3];
+        else if (a == 1) m = c1[w & 3];
+        else {
+          const uint32_t lo = w * 32;
+          const uint32_t valid = ncls - lo >= 32 ? ~0u : ((1u << (ncls - lo)) - 1u);
+          m = ~(c0[w & 3] | c1[w & 3]) & valid;
+        }
+      }
+      smask[threadIdx.x] = m;
+      uint32_t mk = ~m << 1;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        uint32_t mp = mk ^ (mk << 1);
+        mp ^= mp << 2;
+        mp ^= mp << 4;
+        mp ^= mp << 8;
+        mp ^= mp << 16;
+        const uint32_t mv = mp & m;
+        smv[k][threadIdx.x] = mv;
+        m = (m ^ mv) | (mv >> (1 << k));
+        mk &= ~mp;
+      }
+    }
+    __syncthreads();
+    const uint32_t wn = min(128u, nw - w0);
+    for (uint32_t x = 0; x < wn; x += 4) {
+      const uint4 src = __ldg(pl + size_t((w0 + x) >> 2) * rstride + 2 * snp + g);
+      const uint32_t sw[4] = {src.x, src.y, src.z, src.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (x + e >= wn) break;
+        const uint32_t m = smask[x + e];
+        if (m == 0) continue;
+        uint32_t v = sw[e] & m;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const uint32_t t = v & smv[k][x + e];
+          v = (v ^ t) | (t >> (1 << k));
+        }
+        acc |= uint64_t(v) << nacc;
+        nacc += __popc(m);
+        if (nacc >= 32) {
+          emit(uint32_t(acc));
+          acc >>= 32;
+          nacc -= 32;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // flush and zero-pad to the slot's quad count (256-sample stages)
+  if (nacc > 0) emit(uint32_t(acc));
+  while (nq < qout) emit(0u);
+}
+
 // Tile walk within a batch: (i, jb, kb) with jb <= kb < nb(i).
 struct SWalker {
   uint32_t ii, jb, kb, nb;
