@@ -1203,15 +1203,19 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     // bit-compress kernel: one block walks a class's whole sample axis, which
     // pays off while that axis is short; long axes use positions + gather,
     // which parallelise over output quads
-    const bool pext = !ds->old_compact && std::max(ds->N[0], ds->N[1]) <= 16384;
+    const bool pext = !ds->old_compact;
     if (!pext) {
       syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, ds->cstream>>>(d, sa, pbuf);
       if (bt.qmax > 0)
         syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0,
                                       ds->cstream>>>(d, sa, pbuf, ybuf);
     } else {
-      syrk::compact_pext_kernel<<<dim3((bt.rmax + 127) / 128, 4, bt.n), 128, 0, ds->cstream>>>(
-          d, sa, ybuf);
+      // long sample axes: split into segments over a zeroed Y (boundary words ORed)
+      const uint64_t nwmax = (std::max(ds->N[0], ds->N[1]) + 31) / 32;
+      const uint32_t nseg = uint32_t((nwmax + syrk::kPextSeg - 1) / syrk::kPextSeg);
+      if (nseg > 1) CUDA_TRY(cudaMemsetAsync(ybuf, 0, sizeof(uint4) * bt.ytot, ds->cstream));
+      syrk::compact_pext_kernel<<<dim3((bt.rmax + 127) / 128, 4, bt.n * nseg), 128, 0,
+                                  ds->cstream>>>(d, sa, ybuf, nseg);
     }
     CUDA_TRY(cudaEventRecord(ds->ev_cdone[buf], ds->cstream));
     CUDA_TRY(cudaStreamWaitEvent(st, ds->ev_cdone[buf], 0));

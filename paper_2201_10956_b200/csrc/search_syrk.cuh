@@ -231,9 +231,15 @@ __global__ void __launch_bounds__(128) compact_gather_kernel(const DevData d, Sy
 // memory; each row then compresses a source word in 16 ALU ops and appends
 // popc(mask) bits to a 64-bit accumulator that emits 128-bit output quads.
 // Block = 128 rows of one (i, p, c); rows read/write coalesced uint4s.
+// Long sample axes are split into `nseg` segments of kPextSeg source words
+// (grid z = i x segment): a segment starts at the output bit offset given by
+// the popcount of the mask before it, owns its interior output words (plain
+// stores) and ORs its two partial boundary words into a pre-zeroed Y.
+constexpr uint32_t kPextSeg = 256;  // source words (8192 samples) per segment
 __global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, const SyrkArgs s,
-                                                           uint4* __restrict__ Y) {
-  const uint32_t ii = blockIdx.z, p = blockIdx.y >> 1, c = blockIdx.y & 1;
+                                                           uint4* __restrict__ Y, uint32_t nseg) {
+  const uint32_t ii = blockIdx.z / nseg, seg = blockIdx.z % nseg;
+  const uint32_t p = blockIdx.y >> 1, c = blockIdx.y & 1;
   const IInfo* inf = s.info + ii;
   const uint32_t i = s.i_lo + ii;
   const uint32_t R = inf->R;
@@ -246,14 +252,51 @@ __global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, cons
   const uint32_t snp = min(i + 1 + (row >> 1), d.M - 1), g = row & 1;
   const uint32_t ncls = d.n[c];
   const uint32_t nw = (ncls + 31) / 32;  // source words of the class
+  const uint32_t wbeg = seg * kPextSeg, wend = min(nw, wbeg + kPextSeg);
+  if (nseg > 1 && wbeg >= nw) return;
   const size_t rstride = size_t(d.M) * 2;
   const uint4* pl = c ? d.planes[1] : d.planes[0];
   uint4* dst = Y + inf->y_off[p] + size_t(c ? inf->q[p][0] : 0) * R + row;
-  __shared__ uint32_t smv[5][128], smask[128];
+  __shared__ uint32_t smv[5][128], smask[128], sred[4];
+  auto mask_word = [&](uint32_t w) -> uint32_t {
+    const uint4 q0 = __ldg(pl + size_t(w >> 2) * rstride + 2 * i);
+    const uint4 q1 = __ldg(pl + size_t(w >> 2) * rstride + 2 * i + 1);
+    const uint32_t c0[4] = {q0.x, q0.y, q0.z, q0.w}, c1[4] = {q1.x, q1.y, q1.z, q1.w};
+    if (a == 0) return c0[w & 3];
+    if (a == 1) return c1[w & 3];
+    const uint32_t lo = w * 32;
+    const uint32_t valid = ncls - lo >= 32 ? ~0u : ((1u << (ncls - lo)) - 1u);
+    return ~(c0[w & 3] | c1[w & 3]) & valid;
+  };
   uint64_t acc = 0;
   uint32_t nacc = 0, nq = 0, ne = 0;
   uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+  uint32_t kw = 0;       // segmented: output word index of the next emitted word
+  bool first = false;    // segmented: the next emitted word is the shared first word
+  if (nseg > 1) {
+    // output bit offset of this segment = popcount of the mask before it
+    uint32_t cnt = 0;
+    for (uint32_t w = threadIdx.x; w < wbeg; w += 128) cnt += __popc(mask_word(w));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    const uint32_t off = sred[0] + sred[1] + sred[2] + sred[3];
+    kw = off >> 5;
+    nacc = off & 31;
+    first = nacc != 0;
+  }
   auto emit = [&](uint32_t w) {  // uniform across the block: counts depend on the mask only
+    if (nseg > 1) {
+      uint32_t* wp = reinterpret_cast<uint32_t*>(dst + size_t(kw >> 2) * R) + (kw & 3);
+      if (active) {
+        if (first) atomicOr(wp, w);
+        else *wp = w;
+      }
+      first = false;
+      ++kw;
+      return;
+    }
     o0 = o1; o1 = o2; o2 = o3; o3 = w;
     if (++ne == 4) {
       if (active) dst[size_t(nq) * R] = make_uint4(o0, o1, o2, o3);
@@ -261,22 +304,10 @@ __global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, cons
       ne = 0;
     }
   };
-  for (uint32_t w0 = 0; w0 < nw; w0 += 128) {
+  for (uint32_t w0 = wbeg; w0 < wend; w0 += 128) {
     {
       const uint32_t w = w0 + threadIdx.x;
-      uint32_t m = 0;
-      if (w < nw) {
-        const uint4 q0 = __ldg(pl + size_t(w >> 2) * rstride + 2 * i);
-        const uint4 q1 = __ldg(pl + size_t(w >> 2) * rstride + 2 * i + 1);
-        const uint32_t c0[4] = {q0.x, q0.y, q0.z, q0.w}, c1[4] = {q1.x, q1.y, q1.z, q1.w};
-        if (a == 0) m = c0[w & 3];
-        else if (a == 1) m = c1[w & 3];
-        else {
-          const uint32_t lo = w * 32;
-          const uint32_t valid = ncls - lo >= 32 ? ~0u : ((1u << (ncls - lo)) - 1u);
-          m = ~(c0[w & 3] | c1[w & 3]) & valid;
-        }
-      }
+      uint32_t m = w < wend ? mask_word(w) : 0u;
       smask[threadIdx.x] = m;
       uint32_t mk = ~m << 1;
 #pragma unroll
@@ -293,7 +324,7 @@ __global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, cons
       }
     }
     __syncthreads();
-    const uint32_t wn = min(128u, nw - w0);
+    const uint32_t wn = min(128u, wend - w0);
     for (uint32_t x = 0; x < wn; x += 4) {
       const uint4 src = __ldg(pl + size_t((w0 + x) >> 2) * rstride + 2 * snp + g);
       const uint32_t sw[4] = {src.x, src.y, src.z, src.w};
@@ -318,6 +349,14 @@ __global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, cons
       }
     }
     __syncthreads();
+  }
+  if (nseg > 1) {
+    // the last partial word is shared with the next segment; padding is pre-zeroed
+    if (nacc > 0) {
+      first = true;
+      emit(uint32_t(acc));
+    }
+    return;
   }
   // flush and zero-pad to the slot's quad count (256-sample stages)
   if (nacc > 0) emit(uint32_t(acc));
