@@ -638,8 +638,6 @@ struct e3_dataset {
   // compacted (SYRK) engine scratch, allocated on first use
   uint4* y_buf = nullptr;
   size_t y_cap = 0;                   // uint4 elements
-  uint32_t* pos_buf = nullptr;
-  size_t pos_cap = 0;                 // u32 elements
   syrk::IInfo* info_buf = nullptr;
   uint64_t* syrk_off = nullptr;
   size_t info_cap = 0;
@@ -648,7 +646,6 @@ struct e3_dataset {
   size_t smem_optin = 0;
   uint32_t debug_skip = 0;  // E3_DEBUG_SKIP (profiling experiments only)
   bool no_drop = false;     // E3_SYRK_NO_DROP: always compute phases 0 and 1 (A/B testing)
-  bool old_compact = false; // E3_OLD_COMPACT: always positions + gather kernels (A/B testing)
   // scratch reused across searches
   ulonglong2* lists[2] = {nullptr, nullptr};
   uint32_t* counts[2] = {nullptr, nullptr};
@@ -691,7 +688,6 @@ void release(e3_dataset* ds) {
   dfree(ds, ds->itemoff);
   dfree(ds, ds->itemoff_tc);
   dfree(ds, ds->y_buf);
-  dfree(ds, ds->pos_buf);
   dfree(ds, ds->info_buf);
   dfree(ds, ds->syrk_off);
   dfree(ds, ds->scratch);
@@ -950,7 +946,6 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   ds->smem_optin = size_t(smem_optin);
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
-  ds->old_compact = std::getenv("E3_OLD_COMPACT") != nullptr;
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
@@ -1064,13 +1059,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   constexpr size_t kYMax = size_t(16) << 20;     // hard cap (256 MiB per buffer)
   struct Batch {
     uint32_t first, n, rmax, qmax;
-    size_t ytot, ptot;
+    size_t ytot;
     uint64_t tiles, info_at, off_at;
   };
   std::vector<syrk::IInfo> infos;
   std::vector<uint64_t> offs;
   std::vector<Batch> batches;
-  size_t ymax = 0, pmax = 0;
+  size_t ymax = 0;
   for (uint32_t i = i_first; i <= i_last;) {
     Batch bt{};
     bt.first = i;
@@ -1107,10 +1102,6 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
         inf.y_off[a] = bt.ytot;
         bt.ytot += size_t(inf.q[a][0] + inf.q[a][1]) * inf.R;
         bt.qmax = std::max(bt.qmax, inf.q[a][0] + inf.q[a][1]);
-        for (int c = 0; c < 2; ++c) {
-          inf.pos_off[a][c] = bt.ptot;
-          bt.ptot += inf.n[a][c];
-        }
       }
       bt.rmax = std::max(bt.rmax, inf.R);
       infos.push_back(inf);
@@ -1120,7 +1111,6 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     }
     bt.tiles = offs.back();
     ymax = std::max(ymax, bt.ytot);
-    pmax = std::max(pmax, bt.ptot);
     batches.push_back(bt);
   }
   // buffers: Y and positions are double-buffered across consecutive batches so
@@ -1131,12 +1121,6 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     ds->y_buf = nullptr;
     CUDA_TRY(dmalloc(ds, &ds->y_buf, 2 * sizeof(uint4) * std::max<size_t>(ymax, 1)));
     ds->y_cap = ymax;
-  }
-  if (pmax > ds->pos_cap) {
-    dfree(ds, ds->pos_buf);
-    ds->pos_buf = nullptr;
-    CUDA_TRY(dmalloc(ds, &ds->pos_buf, 2 * sizeof(uint32_t) * std::max<size_t>(pmax, 1)));
-    ds->pos_cap = pmax;
   }
   const size_t info_need = infos.size() + offs.size();
   if (info_need > ds->info_cap) {
@@ -1178,7 +1162,6 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     const Batch& bt = batches[b];
     const int buf = int(b & 1);
     uint4* ybuf = ds->y_buf + size_t(buf) * ds->y_cap;
-    uint32_t* pbuf = ds->pos_buf + size_t(buf) * ds->pos_cap;
     syrk::SyrkArgs sa{};
     sa.item_begin = 0;
     sa.item_count = bt.tiles;
@@ -1200,17 +1183,9 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     // batch b's compaction overlaps batch b-1's search; it may reuse buffer
     // b & 1 only once batch b-2's search is done with it
     if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_sdone[buf], 0));
-    // bit-compress kernel: one block walks a class's whole sample axis, which
-    // pays off while that axis is short; long axes use positions + gather,
-    // which parallelise over output quads
-    const bool pext = !ds->old_compact;
-    if (!pext) {
-      syrk::compact_positions_kernel<<<dim3(bt.n, 2, 2), 1024, 0, ds->cstream>>>(d, sa, pbuf);
-      if (bt.qmax > 0)
-        syrk::compact_gather_kernel<<<dim3((bt.rmax + 127) / 128, bt.qmax, bt.n * 2), 128, 0,
-                                      ds->cstream>>>(d, sa, pbuf, ybuf);
-    } else {
-      // long sample axes: split into segments over a zeroed Y (boundary words ORed)
+    {
+      // bit-compress compaction; long sample axes are split into segments
+      // over a zeroed Y (boundary words ORed)
       const uint64_t nwmax = (std::max(ds->N[0], ds->N[1]) + 31) / 32;
       const uint32_t nseg = uint32_t((nwmax + syrk::kPextSeg - 1) / syrk::kPextSeg);
       if (nseg > 1) CUDA_TRY(cudaMemsetAsync(ybuf, 0, sizeof(uint4) * bt.ytot, ds->cstream));
@@ -1232,7 +1207,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ds->ev_sdone[buf], st));
-    *launches += 3;
+    *launches += 2;
   }
   // the host vectors die here: wait for their uploads only (kernels keep running)
   CUDA_TRY(cudaEventSynchronize(ds->ev_upload));

@@ -9,8 +9,8 @@
 // makes every MMA byte useful: 4 (b,g) MACs per compacted sample instead of
 // the masked formulation's 8 over all samples (2.2x less MMA and operand
 // expansion per triplet x sample). Per batch of i's:
-//   compact_positions_kernel  S_{i,a,c} as sorted in-class positions
-//   compact_gather_kernel     Y_{i,a}[quad][row=(j,b)] = X_b^j at S_{i,a,*}
+//   compact_pext_kernel       Y_{i,a}[quad][row=(j,b)] = X_b^j at S_{i,a,*}
+//                             (bit compression by the mask words of SNP i)
 //                             (bit-packed, class 0 quads then class 1 quads,
 //                             each class padded to 256 samples)
 //   search_syrk_kernel        tiles (i, 64-j block, 64-k block), j-block <=
@@ -94,7 +94,6 @@ struct IInfo {
   // ("slots" p = 0, 1: phases lo < hi); the largest phase drop[c] follows
   // exactly from the pair index: T_drop[b][g] = P_jk[b][g] - T_lo - T_hi.
   uint64_t y_off[2];     // uint4 offset of Y_{i,p} (slot p, both classes) in the batch buffer
-  uint64_t pos_off[2][2];// u32 offset of S_{i,phase(p,c),c} in the position buffer
   uint32_t n[2][2];      // |S_{i,phase(p,c),c}|
   uint32_t q[2][2];      // quads of class c in Y_{i,p} (even: 256-sample stages)
   uint32_t R;            // rows = 2 (M - 1 - i)
@@ -118,110 +117,6 @@ struct SyrkArgs {
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
   uint32_t nst;                      // operand stages in use (2..kSStages)
 };
-
-// S_{i,a,c}: block-wide exclusive scan of popcounts over the class words of X_a^i.
-__global__ void __launch_bounds__(1024) compact_positions_kernel(const DevData d, SyrkArgs s,
-                                                                uint32_t* __restrict__ pos) {
-  const uint32_t ii = blockIdx.x, p = blockIdx.y, c = blockIdx.z;
-  const uint32_t i = s.i_lo + ii;
-  const IInfo inf = s.info[ii];
-  uint32_t* out = pos + inf.pos_off[p][c];
-  // slot p holds phase: p + (p >= drop) skipping the dropped one
-  const uint32_t a = (p == 0) ? (inf.drop[c] == 0 ? 1u : 0u) : (inf.drop[c] == 2 ? 1u : 2u);
-  const uint32_t ncls = d.n[c];
-  const uint32_t nw = d.wq[c] * 4;
-  const uint4* pl = c ? d.planes[1] : d.planes[0];
-  const size_t row = size_t(d.M) * 2;
-  __shared__ uint32_t warp_tot[32];
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (uint32_t w0 = 0; w0 < nw; w0 += blockDim.x) {
-    const uint32_t w = w0 + threadIdx.x;
-    uint32_t bits = 0;
-    if (w < nw) {
-      if (a < 2) {
-        const uint4 q = __ldg(pl + size_t(w >> 2) * row + 2 * i + a);
-        const uint32_t comp[4] = {q.x, q.y, q.z, q.w};
-        bits = comp[w & 3];
-      } else {  // genotype 2 = NOT(g0 | g1) on the class's valid samples
-        const uint4 q0 = __ldg(pl + size_t(w >> 2) * row + 2 * i);
-        const uint4 q1 = __ldg(pl + size_t(w >> 2) * row + 2 * i + 1);
-        const uint32_t c0[4] = {q0.x, q0.y, q0.z, q0.w}, c1[4] = {q1.x, q1.y, q1.z, q1.w};
-        const uint32_t lo = w * 32;
-        const uint32_t valid = lo >= ncls ? 0u : (ncls - lo >= 32 ? ~0u : ((1u << (ncls - lo)) - 1u));
-        bits = ~(c0[w & 3] | c1[w & 3]) & valid;
-      }
-    }
-    const uint32_t cnt = __popc(bits);
-    // block exclusive scan of cnt
-    uint32_t incl = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if ((threadIdx.x & 31) >= o) incl += v;
-    }
-    if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      uint32_t t = threadIdx.x < (blockDim.x >> 5) ? warp_tot[threadIdx.x] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, t, o);
-        if (threadIdx.x >= o) t += v;
-      }
-      warp_tot[threadIdx.x] = t;  // inclusive over warps
-    }
-    __syncthreads();
-    const uint32_t wid = threadIdx.x >> 5;
-    uint32_t off = carry + incl - cnt + (wid ? warp_tot[wid - 1] : 0);
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      out[off++] = w * 32 + b;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry += warp_tot[(blockDim.x >> 5) - 1];
-    __syncthreads();
-  }
-}
-
-// Y_{i,a}[q][row] = 128 compacted sample bits of row (j, b), j = i+1+row/2.
-__global__ void __launch_bounds__(128) compact_gather_kernel(const DevData d, SyrkArgs s,
-                                                             const uint32_t* __restrict__ pos,
-                                                             uint4* __restrict__ Y) {
-  const uint32_t ii = blockIdx.z >> 1, a = blockIdx.z & 1;
-  const IInfo inf = s.info[ii];
-  const uint32_t qtot = inf.q[a][0] + inf.q[a][1];
-  const uint32_t q = blockIdx.y;
-  if (q >= qtot) return;
-  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= inf.R) return;
-  const uint32_t i = s.i_lo + ii;
-  const uint32_t c = q < inf.q[a][0] ? 0 : 1;
-  const uint32_t ql = c ? q - inf.q[a][0] : q;
-  const uint32_t n = inf.n[a][c];
-  const uint32_t* P = pos + inf.pos_off[a][c];
-  const uint32_t snp = i + 1 + (row >> 1), g = row & 1;
-  const uint4* pl = (c ? d.planes[1] : d.planes[0]) + 2 * snp + g;
-  const size_t qrow = size_t(d.M) * 2;
-  uint32_t outw[4] = {0, 0, 0, 0};
-  uint32_t cur_q = 0xffffffffu;
-  uint4 cq = make_uint4(0, 0, 0, 0);
-  const uint32_t base = ql * 128;
-  for (uint32_t t = 0; t < 128; ++t) {
-    const uint32_t idx = base + t;
-    if (idx >= n) break;
-    const uint32_t p = __ldg(P + idx);
-    const uint32_t pq = p >> 7;
-    if (pq != cur_q) {
-      cq = __ldg(pl + size_t(pq) * qrow);
-      cur_q = pq;
-    }
-    const uint32_t w = (p >> 5) & 3;
-    const uint32_t word = w == 0 ? cq.x : (w == 1 ? cq.y : (w == 2 ? cq.z : cq.w));
-    outw[t >> 5] |= ((word >> (p & 31)) & 1u) << (t & 31);
-  }
-  Y[inf.y_off[a] + size_t(q) * inf.R + row] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
-}
 
 // Y_{i,p} by bit compression: for slot p (phase a) and class c, every
 // operand row (j, b) keeps the bits of X_b^j at the samples where SNP i has
