@@ -91,6 +91,13 @@ typedef struct {
  * Copies to `device` and builds the marginal index; caller keeps ownership. */
 int e3_dataset_create(uint64_t M, uint64_t N0, uint64_t N1, const uint64_t* ctrl,
                       const uint64_t* cases, int device, e3_dataset** out);
+/* validate (src/datamodel.cpp:28-46) + binarize (src/datamodel.cpp:69-92) on
+ * the device: geno [M][N] u8 SNP-major in {0,1,2}, pheno [N] in {0,1}. Samples
+ * are taken class-contiguous and stable (controls first) exactly like
+ * binarize(), so the dataset equals e3_dataset_create over e3_binarize's
+ * planes; E3_DOMAIN on an out-of-range genotype or phenotype. */
+int e3_dataset_create_genotypes(uint64_t M, uint64_t N, const uint8_t* geno,
+                                const uint8_t* pheno, int device, e3_dataset** out);
 void e3_dataset_destroy(e3_dataset* ds);
 int e3_dataset_info(const e3_dataset* ds, uint64_t* M, uint64_t* N0, uint64_t* N1,
                     int* device);

@@ -551,6 +551,38 @@ __global__ void singles_kernel(const uint4* __restrict__ planes, uint32_t M, uin
 
 // pair[x*M + y] for x < y: {popc(X0x&X0y), popc(X0x&X1y), popc(X1x&X0y), popc(X1x&X1y)}.
 // Per-triple tables / scores through the same marginal derivation as the search.
+// validate + binarize on the device (src/datamodel.cpp:28-46, 69-92): one
+// thread per (SNP m, word-quad q) of a class builds both planes of 128
+// in-class samples straight into the device layout; idx lists the class's
+// samples in order of appearance (the reference's stable class-contiguous
+// reorder), so the planes equal binarize()'s.
+__global__ void binarize_kernel(const uint8_t* __restrict__ geno, uint64_t N, uint32_t M,
+                                const uint32_t* __restrict__ idx, uint32_t n, uint32_t wq,
+                                uint4* __restrict__ planes, uint32_t* bad) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= uint64_t(M) * wq) return;
+  const uint32_t m = uint32_t(t % M), q = uint32_t(t / M);
+  const uint8_t* row = geno + size_t(m) * N;
+  uint32_t p0[4], p1[4], badv = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t a = 0, b = 0;
+    const uint32_t base = q * 128 + w * 32;
+    for (uint32_t u = 0; u < 32; ++u) {
+      if (base + u >= n) break;
+      const uint32_t g = row[__ldg(idx + base + u)];
+      badv |= g > 2;
+      a |= uint32_t(g == 0) << u;
+      b |= uint32_t(g == 1) << u;
+    }
+    p0[w] = a;
+    p1[w] = b;
+  }
+  planes[(size_t(q) * M + m) * 2] = make_uint4(p0[0], p0[1], p0[2], p0[3]);
+  planes[(size_t(q) * M + m) * 2 + 1] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+  if (badv) atomicOr(bad, 1u);
+}
+
 // Class-packed single counts for the narrow SYRK path: {p0: c0 | c1 << 16, p1: ...}.
 __global__ void pack_singles_kernel(const uint2* __restrict__ s0, const uint2* __restrict__ s1,
                                     uint32_t M, uint2* __restrict__ out) {
@@ -795,7 +827,15 @@ std::shared_ptr<const LogTables> log_tables_for(uint64_t N) {
   return t;
 }
 
-int build(e3_dataset* ds, const uint64_t* host[2]) {
+// Host genotype input of e3_dataset_create_genotypes: the matrix goes to the
+// device as bytes and is binarized there.
+struct GenoSrc {
+  const uint8_t* geno = nullptr;   // [M][N]
+  const uint8_t* pheno = nullptr;  // [N]
+  uint64_t N = 0;
+};
+
+int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) {
   // E3_TRACE_CREATE=1: per-phase wall times of dataset creation on stderr
   const bool trace = std::getenv("E3_TRACE_CREATE") != nullptr;
   auto tlast = std::chrono::steady_clock::now();
@@ -834,6 +874,19 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   uint32_t* bad = nullptr;
   CUDA_TRY(dmalloc(ds, &bad, sizeof(uint32_t)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), ds->stream));
+  uint8_t* dgeno = nullptr;
+  uint32_t* didx = nullptr;
+  if (gs) {  // genotype input: the matrix and the in-class sample lists to the device
+    std::vector<uint32_t> idx(gs->N);
+    uint64_t next[2] = {0, ds->N[0]};
+    for (uint64_t j = 0; j < gs->N; ++j) idx[next[gs->pheno[j]]++] = uint32_t(j);
+    CUDA_TRY(dmalloc(ds, &dgeno, size_t(M) * gs->N));
+    CUDA_TRY(dmalloc(ds, &didx, sizeof(uint32_t) * std::max<uint64_t>(gs->N, 1)));
+    CUDA_TRY(cudaMemcpyAsync(dgeno, gs->geno, size_t(M) * gs->N, cudaMemcpyHostToDevice, ds->stream));
+    CUDA_TRY(cudaMemcpyAsync(didx, idx.data(), sizeof(uint32_t) * gs->N, cudaMemcpyHostToDevice,
+                             ds->stream));
+    CUDA_TRY(cudaStreamSynchronize(ds->stream));  // idx is a host temporary
+  }
   for (int c = 0; c < 2; ++c) {
     const uint64_t n = ds->N[c];
     const uint32_t w64 = uint32_t((n + 63) / 64);
@@ -849,19 +902,24 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
       CUDA_TRY(cudaMemsetAsync(ds->single[c], 0, sizeof(uint2) * M, ds->stream));
       continue;  // pairs_tc_kernel writes the (all-zero) pair index
     }
-    uint64_t* raw = nullptr;
-    const size_t raw_bytes = sizeof(uint64_t) * size_t(M) * 2 * w64;
-    CUDA_TRY(dmalloc(ds, &raw, raw_bytes));
-    CUDA_TRY(cudaMemcpyAsync(raw, host[c], raw_bytes, cudaMemcpyHostToDevice, ds->stream));
-    const uint64_t rem = n % 64;
-    const uint64_t tail = rem == 0 ? ~0ull : ((1ull << rem) - 1);
     const uint64_t threads = uint64_t(ds->wq[c]) * M;
-    repack_kernel<<<unsigned((threads + 255) / 256), 256, 0, ds->stream>>>(
-        raw, M, w64, ds->wq[c], tail, ds->planes[c], bad);
+    if (gs) {
+      binarize_kernel<<<unsigned((threads + 255) / 256), 256, 0, ds->stream>>>(
+          dgeno, gs->N, M, didx + (c ? ds->N[0] : 0), uint32_t(n), ds->wq[c], ds->planes[c], bad);
+    } else {
+      uint64_t* raw = nullptr;
+      const size_t raw_bytes = sizeof(uint64_t) * size_t(M) * 2 * w64;
+      CUDA_TRY(dmalloc(ds, &raw, raw_bytes));
+      CUDA_TRY(cudaMemcpyAsync(raw, host[c], raw_bytes, cudaMemcpyHostToDevice, ds->stream));
+      const uint64_t rem = n % 64;
+      const uint64_t tail = rem == 0 ? ~0ull : ((1ull << rem) - 1);
+      repack_kernel<<<unsigned((threads + 255) / 256), 256, 0, ds->stream>>>(
+          raw, M, w64, ds->wq[c], tail, ds->planes[c], bad);
+      dfree(ds, raw);
+    }
     singles_kernel<<<(M + 7) / 8, 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
                                                       ds->single[c]);
     CUDA_TRY(cudaGetLastError());
-    dfree(ds, raw);
   }
   if (ds->narrow) {
     CUDA_TRY(dmalloc(ds, &ds->pairp, sizeof(uint4) * size_t(M) * M));
@@ -869,6 +927,8 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
     pack_singles_kernel<<<(M + 255) / 256, 256, 0, ds->stream>>>(ds->single[0], ds->single[1], M,
                                                                 ds->singlep);
   }
+  dfree(ds, dgeno);
+  dfree(ds, didx);
   mark("planes");
   {
     // marginal pair index of both classes: one tensor-core Gram launch
@@ -964,6 +1024,14 @@ int build(e3_dataset* ds, const uint64_t* host[2]) {
   CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
   CUDA_TRY(cudaStreamSynchronize(ds->stream));
   dfree(ds, bad);
+  if (h_bad && gs) {  // find the first offending genotype for the message (host scan)
+    for (uint64_t i = 0; i < ds->M; ++i)
+      for (uint64_t j = 0; j < gs->N; ++j)
+        if (gs->geno[i * gs->N + j] > 2)
+          return fail(E3_DOMAIN, "genotype value " + std::to_string(gs->geno[i * gs->N + j]) +
+                                     " at snp " + std::to_string(i) + ", sample " +
+                                     std::to_string(j));
+  }
   if (h_bad)
     return fail(E3_DOMAIN,
                 "bit planes violate the dataset invariants (overlapping genotype planes or "
@@ -1018,6 +1086,39 @@ extern "C" int e3_dataset_create(uint64_t M, uint64_t N0, uint64_t N1, const uin
   ds->N[1] = N1;
   const uint64_t* host[2] = {ctrl, cases};
   if (int rc = build(ds, host)) {
+    release(ds);
+    return rc;
+  }
+  *out = ds;
+  return E3_OK;
+}
+
+extern "C" int e3_dataset_create_genotypes(uint64_t M, uint64_t N, const uint8_t* geno,
+                                           const uint8_t* pheno, int device, e3_dataset** out) {
+  *out = nullptr;
+  if (M < 3) return fail(E3_DIMENSION, "need at least 3 SNPs, got " + std::to_string(M));
+  if (M > kMaxSnps) return fail(E3_DOMAIN, "at most 2^21-1 SNPs are supported");
+  if (N == 0) return fail(E3_DIMENSION, "dataset has no samples");
+  if (N > 0xffffffffull) return fail(E3_DOMAIN, "at most 2^32-1 samples are supported");
+  if (!geno || !pheno) return fail(E3_DOMAIN, "missing genotype or phenotype data");
+  uint64_t n1 = 0;
+  for (uint64_t j = 0; j < N; ++j) {  // validate (src/datamodel.cpp:28-46)
+    if (pheno[j] > 1)
+      return fail(E3_DOMAIN, "phenotype value " + std::to_string(pheno[j]) +
+                                 " at snp 0, sample " + std::to_string(j));
+    n1 += pheno[j];
+  }
+  e3_dataset* ds = new e3_dataset;
+  ds->device = device;
+  ds->M = M;
+  ds->N[0] = N - n1;
+  ds->N[1] = n1;
+  GenoSrc gs;
+  gs.geno = geno;
+  gs.pheno = pheno;
+  gs.N = N;
+  const uint64_t* host[2] = {nullptr, nullptr};
+  if (int rc = build(ds, host, &gs)) {
     release(ds);
     return rc;
   }

@@ -106,6 +106,7 @@ _U32 = C.c_uint32
 # name -> (restype, argtypes); every symbol declared in include/epi3cu.h
 SIGNATURES = {
     "e3_dataset_create": (C.c_int, [_U64, _U64, _U64, _P, _P, C.c_int, C.POINTER(_P)]),
+    "e3_dataset_create_genotypes": (C.c_int, [_U64, _U64, _P, _P, C.c_int, C.POINTER(_P)]),
     "e3_dataset_destroy": (None, [_P]),
     "e3_dataset_info": (C.c_int, [_P, _P, _P, _P, _P]),
     "e3_search": (C.c_int, [_P, C.POINTER(e3_search_cfg), _P, C.POINTER(_U32),
@@ -403,6 +404,26 @@ class DeviceDataset:
         _check(lib.e3_dataset_create(ds.num_snps, ds.num_controls, ds.num_cases, ctrl, cases,
                                      device, C.byref(h)))
         self._h = h
+
+    @classmethod
+    def from_genotypes(cls, geno: np.ndarray, pheno: np.ndarray, device: int = 0) -> "DeviceDataset":
+        """validate + binarize (src/datamodel.cpp:28-46, 69-92) on the device
+        from a [M, N] uint8 genotype matrix and [N] phenotypes; equal to
+        DeviceDataset(binarize(geno, pheno))."""
+        geno = np.ascontiguousarray(geno, dtype=np.uint8)
+        pheno = np.ascontiguousarray(pheno, dtype=np.uint8)
+        M, N = geno.shape
+        if pheno.shape != (N,):
+            raise DimensionError(f"phenotype length {pheno.shape} != {N} samples")
+        h = C.c_void_p()
+        _check(lib.e3_dataset_create_genotypes(M, N, _ptr(geno), _ptr(pheno), device, C.byref(h)))
+        self = cls.__new__(cls)
+        self.num_snps = M
+        self.num_cases = int(pheno.sum())
+        self.num_controls = N - self.num_cases
+        self.device = device
+        self._h = h
+        return self
 
     @property
     def handle(self):

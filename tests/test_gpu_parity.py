@@ -235,3 +235,33 @@ def test_syrk_code_paths_match_oracle(monkeypatch, env, M, n0, n1, seed):
     with epi3.DeviceDataset(ds) as dd:
         got = hits_of(dd.search(epi3.SearchConfig(top_k=12, engine="syrk")))
     assert_hits_identical(got, po.OracleDataset.of(ds).search(top_k=12))
+
+
+@pytest.mark.parametrize("M,n0,n1,seed", [(30, 517, 260, 31), (12, 0, 300, 32), (9, 20001, 3, 33)])
+def test_device_binarize_matches_host(M, n0, n1, seed):
+    """e3_dataset_create_genotypes (binarize on the device) builds the same
+    dataset as host binarize + e3_dataset_create: identical tables and top-k."""
+    rng = np.random.default_rng(seed)
+    geno = rng.integers(0, 3, (M, n0 + n1), dtype=np.uint8)
+    pheno = np.array([0] * n0 + [1] * n1, dtype=np.uint8)
+    rng.shuffle(pheno)
+    ds = epi3.binarize(geno, pheno)
+    triples = [(a, b, c) for a in range(M) for b in range(a + 1, M) for c in range(b + 1, M)]
+    with epi3.DeviceDataset(ds) as host_built, epi3.DeviceDataset.from_genotypes(geno, pheno) as dev_built:
+        assert (dev_built.tables(triples) == host_built.tables(triples)).all()
+        assert_hits_identical(hits_of(dev_built.search(epi3.SearchConfig(top_k=8))),
+                              hits_of(host_built.search(epi3.SearchConfig(top_k=8))))
+    assert_hits_identical(hits_of(epi3.DeviceDataset.from_genotypes(geno, pheno).search(
+        epi3.SearchConfig(top_k=8))), po.OracleDataset.of(ds).search(top_k=8))
+
+
+def test_device_binarize_rejects_bad_values():
+    geno = np.zeros((4, 10), dtype=np.uint8)
+    pheno = np.array([0, 1] * 5, dtype=np.uint8)
+    geno[2, 7] = 3
+    with pytest.raises(epi3.DomainError, match="snp 2, sample 7"):
+        epi3.DeviceDataset.from_genotypes(geno, pheno)
+    geno[2, 7] = 1
+    pheno[4] = 2
+    with pytest.raises(epi3.DomainError):
+        epi3.DeviceDataset.from_genotypes(geno, pheno)
