@@ -186,6 +186,20 @@ __device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_
   return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
 }
 
+// k2_screen_packed for counts scaled by 4 (word = 4 r0 | 4 r1 << 16): the
+// halves are the table byte offsets of G[r0], G[r1], and their sum + 4 that
+// of G[r0 + r1 + 1].
+__device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_s) {
+  float s[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 27; ++c) {
+    const uint32_t a0 = G_s + (n[c] & 0xffffu), o1 = n[c] >> 16;
+    const float t = __fsub_rn(__fsub_rn(lds_f32(a0 + o1 + 4), lds_f32(a0)), lds_f32(G_s + o1));
+    s[c % 3] = __fadd_rn(s[c % 3], t);
+  }
+  return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
+}
+
 // fp32 screen of k2_score: sum_c (G[r0+r1+1] - G[r0]) - G[r1] over a
 // shared-memory table G[n] = fl32(P[n] - alpha*n). The affine shift cancels
 // per cell up to the constant alpha, so score = screen + 27*alpha up to an
@@ -585,11 +599,11 @@ __global__ void binarize_kernel(const uint8_t* __restrict__ geno, uint64_t N, ui
 
 // Class-packed single counts for the narrow SYRK path: {p0: c0 | c1 << 16, p1: ...}.
 __global__ void pack_singles_kernel(const uint2* __restrict__ s0, const uint2* __restrict__ s1,
-                                    uint32_t M, uint2* __restrict__ out) {
+                                    uint32_t M, uint32_t sh, uint2* __restrict__ out) {
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= M) return;
   const uint2 a = s0[x], b = s1[x];
-  out[x] = make_uint2(a.x | (b.x << 16), a.y | (b.y << 16));
+  out[x] = make_uint2((a.x << sh) | (b.x << (16 + sh)), (a.y << sh) | (b.y << (16 + sh)));
 }
 
 // POPC pair index, used only when a class holds >= 2^23 samples (beyond the
@@ -658,6 +672,7 @@ struct e3_dataset {
   uint4* pairp = nullptr;    // narrow class-packed mirrored pair index (every N_c < 2^16)
   uint2* singlep = nullptr;  // narrow class-packed single counts
   bool narrow = false;
+  uint32_t shift = 0;  // narrow: packed counts scaled by 1 << shift (2 when every N_c < 2^14)
   double* logp = nullptr;
   float* ktab = nullptr;              // K2 screening table (see k2_screen)
   uint32_t ktab_n = 0;
@@ -767,7 +782,7 @@ DevData dev_view(const e3_dataset* ds) {
   d.itemoff = ds->itemoff;
   d.pairp = ds->pairp;
   d.singlep = ds->singlep;
-  d.npk = uint32_t(ds->N[0]) | (uint32_t(ds->N[1]) << 16);
+  d.npk = (uint32_t(ds->N[0]) << ds->shift) | (uint32_t(ds->N[1]) << (16 + ds->shift));
   d.ktab = ds->ktab;
   d.ktab_n = ds->ktab_n;
   d.kshift = ds->kshift;
@@ -871,6 +886,8 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   ds->num_sms = n_sms;
   const uint32_t M = uint32_t(ds->M);
   ds->narrow = std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 16) && !std::getenv("E3_NO_NARROW");
+  ds->shift = ds->narrow && std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 14) &&
+                      !std::getenv("E3_NO_SCALED") ? 2u : 0u;
   uint32_t* bad = nullptr;
   CUDA_TRY(dmalloc(ds, &bad, sizeof(uint32_t)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), ds->stream));
@@ -925,7 +942,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
     CUDA_TRY(dmalloc(ds, &ds->pairp, sizeof(uint4) * size_t(M) * M));
     CUDA_TRY(dmalloc(ds, &ds->singlep, sizeof(uint2) * M));
     pack_singles_kernel<<<(M + 255) / 256, 256, 0, ds->stream>>>(ds->single[0], ds->single[1], M,
-                                                                ds->singlep);
+                                                                ds->shift, ds->singlep);
   }
   dfree(ds, dgeno);
   dfree(ds, didx);
@@ -937,6 +954,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
     pa.nb = (M + pairs_tc::kBlk - 1) / pairs_tc::kBlk;
     pa.tiles = uint64_t(pa.nb) * (pa.nb + 1) / 2;
     pa.pairp = ds->pairp;
+    pa.shift = ds->shift;
     for (int c = 0; c < 2; ++c) {
       pa.wq[c] = ds->wq[c];
       pa.planes[c] = ds->planes[c];
@@ -1006,16 +1024,22 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   ds->smem_optin = size_t(smem_optin);
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, false>,
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 0>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, false>,
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 0>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, true>,
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 1>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, true>,
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 1>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 2048)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 2>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 2048)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
@@ -1299,12 +1323,15 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     // checks; the others run the unranged kernel
     const uint64_t b_lo = first_rank(bt.first), b_hi = first_rank(bt.first + bt.n);
     const bool part = ranged && (r0 > b_lo || r1 < b_hi);
-    if (ds->narrow) {
-      if (part) syrk::search_syrk_kernel<true, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
-      else syrk::search_syrk_kernel<false, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    if (ds->narrow && ds->shift) {
+      if (part) syrk::search_syrk_kernel<true, 2><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, 2><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    } else if (ds->narrow) {
+      if (part) syrk::search_syrk_kernel<true, 1><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, 1><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     } else {
-      if (part) syrk::search_syrk_kernel<true, false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
-      else syrk::search_syrk_kernel<false, false><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      if (part) syrk::search_syrk_kernel<true, 0><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, 0><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ds->ev_sdone[buf], st));

@@ -34,6 +34,7 @@ struct PArgs {
   uint4* pair[2];           // [M * M] wide (u32) counts
   uint4* pairp;             // [M * M] narrow class-packed mirror (c0 | c1 << 16), every N_c < 2^16
   uint64_t tiles;           // nb (nb + 1) / 2 tiles; each = two units (class 0, class 1)
+  uint32_t shift;           // narrow: packed counts scaled by 1 << shift
 };
 
 // tile -> (x-block, y-block), row-major triangle xb <= yb
@@ -214,7 +215,9 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
               *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[0] + up) + 2 * a) = w0;
               *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[1] + up) + 2 * a) = w1;
               if (kNarrow) {
-                const uint2 pk = make_uint2(w0.x | (w1.x << 16), w0.y | (w1.y << 16));
+                const uint32_t sh = p.shift;
+                const uint2 pk = make_uint2((w0.x << sh) | (w1.x << (16 + sh)),
+                                            (w0.y << sh) | (w1.y << (16 + sh)));
                 *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pairp + up) + 2 * a) = pk;
                 *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pairp + lo) + 2 * a) = pk;
               } else {

@@ -291,8 +291,13 @@ struct SWalker {
 // singles — and the dropped-phase recovery and the table derivation run on
 // both classes at once (every intermediate is a true count, so the packed
 // 32-bit arithmetic never carries or borrows across the halves).
-template <bool kRanged, bool kNarrow>
+// kMode: 0 = wide, 1 = narrow, 2 = narrow with counts scaled by 4 (every
+// class < 2^14 samples): a packed word then holds the byte offsets of its two
+// counts in the screening table, which saves the index arithmetic per lookup.
+template <bool kRanged, int kMode>
 __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
+  constexpr bool kNarrow = kMode >= 1;
+  constexpr uint32_t kSh = kMode == 2 ? 2u : 0u;  // count scale shift of packed words
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               for (int x = 0; x < 16; ++x) {
                 const int m = m2 + (x >> 3), tg = x & 7;
                 scr[(a * kRounds * 8 + m * 8 + tg) * 256] =
-                    (f32_count(v0[x]) & keep0) | ((f32_count(v1[x]) & keep1) << 16);
+                    ((f32_count(v0[x]) & keep0) << kSh) | ((f32_count(v1[x]) & keep1) << (16 + kSh));
               }
             }
             fence_before();
@@ -641,7 +646,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 if (s.debug_skip & 4)
                   pass[h] = n[26] == 0x7fffffffu;  // profiling: derivation only
                 else
-                  pass[h] = valid[h] && (!s.screen || k2_screen_packed(n, ktab_s) <= thr_f);
+                  pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled(n, ktab_s)
+                                                              : k2_screen_packed(n, ktab_s)) <= thr_f);
               }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
@@ -650,8 +656,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                   derive_cells(T[h], pij, pik[h], pjk[h], sip, sjp, skp[h], d.npk, n);
 #pragma unroll
                   for (int c = 0; c < 27; ++c) {
-                    n0[c] = n[c] & 0xffffu;
-                    n1[c] = n[c] >> 16;
+                    n0[c] = (n[c] & 0xffffu) >> kSh;
+                    n1[c] = n[c] >> (16 + kSh);
                   }
                   sk[h] = score_key(k2_device(n0, n1, d.logp));
                   tk[h] = triple_key(i, j, kk[h]);

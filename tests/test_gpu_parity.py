@@ -221,7 +221,7 @@ def test_class_beyond_exact_f32_range():
     assert_hits_identical(got, od.search(top_k=4))
 
 
-@pytest.mark.parametrize("env", [{}, {"E3_NO_NARROW": "1"}, {"E3_NO_SCREEN": "1"},
+@pytest.mark.parametrize("env", [{}, {"E3_NO_NARROW": "1"}, {"E3_NO_SCREEN": "1"}, {"E3_NO_SCALED": "1"},
                                  {"E3_SYRK_STAGES": "2"}, {"E3_SYRK_NO_DROP": "1"},
                                  {"E3_NO_NARROW": "1", "E3_NO_SCREEN": "1"}])
 @pytest.mark.parametrize("M,n0,n1,seed", [(48, 700, 333, 21), (20, 20000, 9000, 22)])
