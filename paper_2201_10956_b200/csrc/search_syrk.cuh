@@ -113,7 +113,8 @@ struct SyrkArgs {
   const uint64_t* itemoff;           // [n_i + 1] tile prefix within the batch
   const uint4* Y;
   uint32_t* scratch;                 // [grid][kRounds * 16][256]
-  uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no K2, 2 = no expansion
+  uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no scoring, 2 = no
+                                     // operand expansion, 4 = derivation without the screen
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
   uint32_t nst;                      // operand stages in use (2..kSStages)
 };
