@@ -63,11 +63,14 @@ typedef struct {
 
 #define E3_MAX_TOP_K 256u
 /* Engine selection (e3_search_cfg.flags). All engines produce identical
- * results; 0 = auto (E3_ENGINE_SYRK for N >= 4096 samples, else
- * E3_ENGINE_TC_MASKED).
+ * results; 0 = auto (E3_ENGINE_SYRK for N >= 4096 samples with every class
+ * < 2^23 samples, else E3_ENGINE_TC_MASKED).
  *   E3_ENGINE_POPC       LOP3/POPC kernel (marginal subtraction + carry-save)
  *   E3_ENGINE_TC_MASKED  tcgen05 kind::i8 GEMM: pair products x singles
- *   E3_ENGINE_SYRK       per-first-SNP sample compaction + tcgen05 kind::i8 SYRK */
+ *   E3_ENGINE_SYRK       per-first-SNP sample compaction (two smaller genotype
+ *                        phases) + tcgen05 kind::mxf4 SYRK on packed 0/1 E2M1
+ *                        operands, fp32 K2 screen + exact fp64 K2; E3_DOMAIN
+ *                        when a class holds >= 2^23 samples */
 #define E3_ENGINE_POPC 1u
 #define E3_ENGINE_TC_MASKED 2u
 #define E3_ENGINE_SYRK 3u
