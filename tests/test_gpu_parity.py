@@ -265,3 +265,13 @@ def test_device_binarize_rejects_bad_values():
     pheno[4] = 2
     with pytest.raises(epi3.DomainError):
         epi3.DeviceDataset.from_genotypes(geno, pheno)
+
+
+@pytest.mark.parametrize("engine", ["syrk", "tc_masked", "popc"])
+@pytest.mark.parametrize("M", [3, 4, 65, 66, 130])
+def test_snp_block_edges(engine, M):
+    """Smallest searches and SNP counts around the 64-SNP tile blocks."""
+    ds = _random_ds(M, 301, 257, 40 + M)
+    with epi3.DeviceDataset(ds) as dd:
+        got = hits_of(dd.search(epi3.SearchConfig(top_k=7, engine=engine)))
+    assert_hits_identical(got, po.OracleDataset.of(ds).search(top_k=7))
