@@ -157,6 +157,9 @@ struct SearchResult {
 bool same_outcome(const SearchResult& a, const SearchResult& b);
 std::uint64_t num_combinations(std::uint64_t m, std::uint64_t k);
 SearchResult run_search(const BitPlaneDataset& ds, const SearchConfig& cfg);
+// Same search starting from a genotype matrix: validate + binarize run on each
+// device (e3_dataset_create_genotypes) instead of the host.
+SearchResult run_search(const GenotypeMatrix& m, const SearchConfig& cfg);
 SearchResult reduce_results(std::span<const SearchResult> partials);
 
 // ---- per-triple tables (kernels.hpp:75) -----------------------------------------------
@@ -166,6 +169,8 @@ FrequencyTable freq_table_reduced(const BitPlaneDataset& ds, Triple t);
 class DeviceDataset {
  public:
   explicit DeviceDataset(const BitPlaneDataset& ds, int device = 0);
+  // validate + binarize on the device (same dataset as from binarize(m))
+  explicit DeviceDataset(const GenotypeMatrix& m, int device = 0);
   ~DeviceDataset();
   DeviceDataset(const DeviceDataset&) = delete;
   DeviceDataset& operator=(const DeviceDataset&) = delete;

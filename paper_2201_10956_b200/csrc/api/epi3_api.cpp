@@ -253,6 +253,13 @@ DeviceDataset::DeviceDataset(const BitPlaneDataset& ds, int device) : m_(ds.num_
                           ds.data(1).data(), device, &h_));
 }
 
+DeviceDataset::DeviceDataset(const GenotypeMatrix& m, int device) : m_(m.num_snps) {
+  if (m.genotypes.size() != m.num_snps * m.num_samples || m.phenotype.size() != m.num_samples)
+    throw DimensionError("genotype matrix size does not match its dimensions");
+  check(e3_dataset_create_genotypes(m.num_snps, m.num_samples, m.genotypes.data(),
+                                    m.phenotype.data(), device, &h_));
+}
+
 DeviceDataset::~DeviceDataset() { e3_dataset_destroy(h_); }
 
 SearchResult DeviceDataset::search(std::uint32_t top_k, std::uint64_t r0, std::uint64_t r1) const {
@@ -307,15 +314,17 @@ SearchResult reduce_results(std::span<const SearchResult> partials) {
   return out;
 }
 
-// run_search (search.cpp:127-250): one host thread per GPU, each with a
-// replicated dataset and an equal-work triple-rank range; partials merged by
-// reduce_results exactly as the reference merges its worker partials.
-SearchResult run_search(const BitPlaneDataset& ds, const SearchConfig& cfg) {
-  if (ds.num_snps() < 3) throw DimensionError("search needs at least 3 SNPs");
+namespace {
+// The body of run_search over any dataset source: one host thread per GPU,
+// each building its replicated DeviceDataset and searching an equal-work
+// triple-rank range; partials merged by reduce_results.
+template <typename Source>
+SearchResult run_search_impl(const Source& src, std::size_t num_snps, const SearchConfig& cfg) {
+  if (num_snps < 3) throw DimensionError("search needs at least 3 SNPs");
   if (cfg.top_k < 1) throw DomainError("top_k must be >= 1");
   if (cfg.devices.empty()) throw DomainError("at least one device is required");
   const auto t0 = std::chrono::steady_clock::now();
-  const std::uint64_t total = num_combinations(ds.num_snps(), 3);
+  const std::uint64_t total = num_combinations(num_snps, 3);
   const std::uint64_t r0 = cfg.rank_begin;
   const std::uint64_t r1 = cfg.rank_end == 0 ? total : cfg.rank_end;
   if (r1 > total || r0 > r1) throw IndexError("triple-rank range outside [0, C(M,3))");
@@ -325,7 +334,7 @@ SearchResult run_search(const BitPlaneDataset& ds, const SearchConfig& cfg) {
   auto worker = [&](std::size_t g) {
     try {
       const std::uint64_t a = r0 + (r1 - r0) * g / G, b = r0 + (r1 - r0) * (g + 1) / G;
-      DeviceDataset dd(ds, cfg.devices[g]);
+      DeviceDataset dd(src, cfg.devices[g]);
       partials[g] = a < b ? dd.search(cfg.top_k, a, b) : SearchResult{};
       partials[g].top_k = cfg.top_k;
       if (a == b) partials[g].best = Hit{std::numeric_limits<double>::infinity(), Triple{}};
@@ -347,6 +356,18 @@ SearchResult run_search(const BitPlaneDataset& ds, const SearchConfig& cfg) {
   r.stats.elapsed_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return r;
+}
+}  // namespace
+
+// run_search (search.cpp:127-250): one host thread per GPU, each with a
+// replicated dataset and an equal-work triple-rank range; partials merged by
+// reduce_results exactly as the reference merges its worker partials.
+SearchResult run_search(const BitPlaneDataset& ds, const SearchConfig& cfg) {
+  return run_search_impl(ds, ds.num_snps(), cfg);
+}
+
+SearchResult run_search(const GenotypeMatrix& m, const SearchConfig& cfg) {
+  return run_search_impl(m, m.num_snps, cfg);
 }
 
 FrequencyTable freq_table_reduced(const BitPlaneDataset& ds, Triple t) {

@@ -79,11 +79,30 @@ int cmd_generate(const Args& a) {
 }
 
 int cmd_detect(const Args& a) {
-  const BitPlaneDataset ds = load(a.get("in"));
+  // packed input: the bit planes go to the GPU as they are; text input: the
+  // genotype matrix is validated and binarized on the GPU
   SearchConfig cfg;
   cfg.top_k = std::uint32_t(a.num("top-k", 10));
   cfg.devices = devices(a);
-  const SearchResult r = run_search(ds, cfg);
+  struct Dims {
+    std::size_t snps, samples, controls, cases;
+    std::size_t num_snps() const { return snps; }
+    std::size_t num_samples() const { return samples; }
+    std::size_t num_controls() const { return controls; }
+    std::size_t num_cases() const { return cases; }
+  } ds{};
+  SearchResult r;
+  if (is_packed_file(a.get("in"))) {
+    const BitPlaneDataset bp = read_packed(a.get("in"));
+    ds = {bp.num_snps(), bp.num_samples(), bp.num_controls(), bp.num_cases()};
+    r = run_search(bp, cfg);
+  } else {
+    const GenotypeMatrix gm = read_text(a.get("in"));
+    validate(gm);
+    const auto n1 = std::size_t(std::count(gm.phenotype.begin(), gm.phenotype.end(), std::uint8_t{1}));
+    ds = {gm.num_snps, gm.num_samples, gm.num_samples - n1, n1};
+    r = run_search(gm, cfg);
+  }
   if (a.has("json")) {
     std::printf("{\"input\": \"%s\", \"snps\": %zu, \"samples\": %zu, \"controls\": %zu, "
                 "\"cases\": %zu, \"engine\": \"b200\", \"gpus\": %zu, \"best\": {\"score\": %.17g, "

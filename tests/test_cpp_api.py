@@ -80,3 +80,21 @@ def test_cli_verify_and_bench():
                             "--format", "json"], capture_output=True, text=True, check=True)
         rep = json.loads(r.stdout)
         assert rep["elements"] == epi3.num_combinations(24, 3) * 700 and rep["eps"] > 0
+
+
+@pytest.mark.gpu
+def test_cli_detect_text_input_binarizes_on_device():
+    """A text genotype file goes through run_search(GenotypeMatrix) (binarize on
+    the GPU) and reports exactly what the packed file of the same data does."""
+    with tempfile.TemporaryDirectory() as d:
+        t, p = Path(d) / "g.txt", Path(d) / "g.epi3"
+        for out, fmt in ((t, "text"), (p, "packed")):
+            subprocess.run([str(build.CLI), "generate", "--snps", "40", "--samples", "900",
+                            "--seed", "9", "--plant", "4,17,31", "--format", fmt, "--out", str(out)],
+                           check=True, capture_output=True)
+        rt = json.loads(subprocess.run([str(build.CLI), "detect", "--in", str(t), "--json"],
+                                       capture_output=True, text=True, check=True).stdout)
+        rp = json.loads(subprocess.run([str(build.CLI), "detect", "--in", str(p), "--json"],
+                                       capture_output=True, text=True, check=True).stdout)
+        for k in ("snps", "samples", "controls", "cases", "best", "top"):
+            assert rt[k] == rp[k], k
