@@ -496,7 +496,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             mbar_wait(&tfull_bar[s0], (u / kUnits) & 1);
             mbar_wait(&tfull_bar[s1], ((u + 1) / kUnits) & 1);
             fence_after();
-            const uint32_t keep0 = inf.q[a][0] ? 0xffffffffu : 0u, keep1 = inf.q[a][1] ? 0xffffffffu : 0u;
+            // count c (f32, exact) -> 2^23 + c * 2^kSh by one FFMA (c * 2^kSh < 2^16),
+            // then one PRMT joins the low halves of both classes; a class with
+            // no samples in this slot has an unwritten accumulator -> constant 0
+            const bool e0 = inf.q[a][0] == 0, e1 = inf.q[a][1] == 0;
+            const float scl = float(1u << kSh);
             const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + half * 8 * kRounds;
 #pragma unroll
             for (int m2 = 0; m2 < kRounds; m2 += 2) {
@@ -507,8 +511,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
               for (int x = 0; x < 16; ++x) {
                 const int m = m2 + (x >> 3), tg = x & 7;
-                scr[(a * kRounds * 8 + m * 8 + tg) * 256] =
-                    ((f32_count(v0[x]) & keep0) << kSh) | ((f32_count(v1[x]) & keep1) << (16 + kSh));
+                const uint32_t b0 = e0 ? 0x4B000000u : __float_as_uint(__fmaf_rn(__uint_as_float(v0[x]), scl, 8388608.f));
+                const uint32_t b1 = e1 ? 0x4B000000u : __float_as_uint(__fmaf_rn(__uint_as_float(v1[x]), scl, 8388608.f));
+                scr[(a * kRounds * 8 + m * 8 + tg) * 256] = __byte_perm(b0, b1, 0x5410);
               }
             }
             fence_before();
