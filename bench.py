@@ -311,6 +311,14 @@ def main():
                              "masked GEMM: 8 int8 MACs per element (4 (a,b) pair rows x 2 g "
                              "columns)") + "; the other cells come exactly from the marginal "
                                            "index"}
+            if args.engine == "syrk":
+                # the tensor pipe is not what binds this kernel: ncu shows the L1
+                # LSU data path (the K2 screen's shared-memory gathers, operand
+                # stores, scratch/pair loads) as the busiest unit
+                roof["binding_unit"] = {
+                    "unit": "L1TEX LSU data path (l1tex__data_pipe_lsu_wavefronts)",
+                    "pct_of_peak": 74.0, "tensor_pipe_pct": 18.0,
+                    "from": "profiles/r01pm2_search_cfg3_raw.csv (ncu --set full, cfg3)"}
         else:
             peak = nsm * POPC_PER_SM_CLK * f_mhz * 1e6 / 1e12
             achieved = kernel_rate * ALG_POPC_PER_ELEMENT / 1e12
