@@ -107,6 +107,7 @@ struct DevData {
   const float* ktab;         // screening table G[n] = fl32(logp[n] - alpha*n), ktab_n entries
   uint32_t ktab_n;           // N+2 rounded up to a multiple of 4
   double kshift;             // -27*alpha + proven screening error bound
+  float st_c1;               // stirling_term slope -(1+alpha) (k2_screen_packed)
 };
 
 // ------------------------------------------------------------------------
@@ -173,13 +174,31 @@ __device__ __forceinline__ float lds_f32(uint32_t saddr) {
   asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
   return v;
 }
+// The P[r0+r1+1] term of a cell from Stirling's lower bound instead of a
+// table lookup: ln m! >= (m+1/2) ln m - m + ln(2 pi)/2 for every m >= 1
+// (the remainder lies in (1/(12m+1), 1/(12m))), so the screen can only fall
+// (never miss a triple); its fp32 + lg2.approx error is in the host margin
+// (k2_screen_margin). T = ln2 (m+1/2) lg2(m) + c1 m + ln(2 pi)/2 with
+// c1 = -(1+alpha) (the G table's shift included): one MUFU + 4 FP instead of
+// a bank-conflicted shared-memory gather and its address arithmetic.
+constexpr float kLn2 = 0.693147180559945309f;
+constexpr float kHalfLn2Pi = 0.918938533204672742f;
+__device__ __forceinline__ float stirling_term(uint32_t mbits, float c1) {
+  const float m = __fsub_rn(__uint_as_float(mbits), 8388608.f);  // mbits = bits of 2^23 + m
+  float lg;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(m));
+  const float ap = __fmaf_rn(m, kLn2, 0.5f * kLn2);
+  const float cp = __fmaf_rn(m, c1, kHalfLn2Pi);
+  return __fmaf_rn(ap, lg, cp);
+}
+
 // k2_screen on class-packed cells (narrow path): word = class0 | class1 << 16.
-__device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_s) {
+__device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_s, float c1) {
   float s[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int c = 0; c < 27; ++c) {
     const uint32_t r0 = n[c] & 0xffffu, r1 = n[c] >> 16;
-    const float t = __fsub_rn(__fsub_rn(lds_f32(G_s + 4 * (r0 + r1 + 1)), lds_f32(G_s + 4 * r0)),
+    const float t = __fsub_rn(__fsub_rn(stirling_term(r0 + r1 + 0x4B000001u, c1), lds_f32(G_s + 4 * r0)),
                               lds_f32(G_s + 4 * r1));
     s[c % 3] = __fadd_rn(s[c % 3], t);
   }
@@ -188,7 +207,10 @@ __device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_
 
 // k2_screen_packed for counts scaled by 4 (word = 4 r0 | 4 r1 << 16): the
 // halves are the table byte offsets of G[r0], G[r1], and their sum + 4 that
-// of G[r0 + r1 + 1].
+// of G[r0 + r1 + 1]. All three terms stay table lookups here: the address
+// arithmetic is free, and stirling_term's extra FP/MUFU issue cost more than
+// the bank conflicts it saves (measured: cfg3 -6.5%, cfg2 -11%), whereas the
+// unscaled k2_screen_packed gains (cfg5 +1.6%).
 __device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_s) {
   float s[3] = {0.f, 0.f, 0.f};
 #pragma unroll
@@ -677,6 +699,7 @@ struct e3_dataset {
   float* ktab = nullptr;              // K2 screening table (see k2_screen)
   uint32_t ktab_n = 0;
   double kshift = 0;
+  float st_c1 = 0.f;
   uint64_t* itemoff = nullptr;
   std::vector<uint64_t> h_itemoff;
   uint64_t* itemoff_tc = nullptr;     // tensor-core kernel item prefix (32-j x 64-k tiles)
@@ -786,6 +809,7 @@ DevData dev_view(const e3_dataset* ds) {
   d.ktab = ds->ktab;
   d.ktab_n = ds->ktab_n;
   d.kshift = ds->kshift;
+  d.st_c1 = ds->st_c1;
   return d;
 }
 
@@ -797,11 +821,20 @@ DevData dev_view(const e3_dataset* ds) {
 // sum_c log((n_c+1) C(n_c, r0)) <= N ln 2 + 27 ln(N+1), each term >= 0, and
 // the shifted terms subtract alpha. Doubled, plus slack for the fp64
 // rounding of the reference score itself.
+//
+// k2_screen_packed replaces the P[m] lookup (m = r0+r1+1) by stirling_term,
+// a lower bound, so only its computed-above-exact error counts. Per cell, with
+// lg2.approx absolute error E <= 2^-20 (4x the PTX bound) and |lg2 x| <= L:
+// |ap - ap*| |lg| + ap* E + |cp - cp*| + u|T| <= (m+1/2)(2.1 u ln2 L + ln2 E)
+// + 2.1 u (3 + alpha) m + u (gmax + 5); summed with sum_c m = N + 27.
 double k2_screen_margin(double gmax, double N, double alpha) {
   const double u = std::ldexp(1.0, -24);
   const double smax = N * std::log(2.0) + 27.0 * std::log(N + 1.0) + 27.0 * std::fabs(alpha) + 1.0;
   const double per_cell = u * (3.0 * gmax + 2.0 * gmax + 3.0 * gmax + smax) * (1.0 + 4.0 * u);
-  return 2.0 * 27.0 * per_cell + 1e-9 * smax + 1e-6;
+  const double L = std::log2(4.0 * (N + 2.0)), E = std::ldexp(1.0, -20), ln2 = std::log(2.0);
+  const double stirling = (N + 41.0) * (2.1 * u * ln2 * L + ln2 * E) +
+                          2.1 * u * (3.0 + std::fabs(alpha)) * (N + 27.0) + 27.0 * u * (gmax + 5.0);
+  return 2.0 * (27.0 * per_cell + stirling) + 1e-9 * smax + 1e-6;
 }
 
 // Host tables that depend only on N: the reference's log table (built exactly
@@ -815,6 +848,7 @@ struct LogTables {
   std::vector<double> logp;  // N+2 entries
   std::vector<float> ktab;   // N+2 rounded up to a multiple of 4
   double kshift = 0;
+  float st_c1 = 0.f;  // stirling_term slope -(1+alpha)
 };
 std::shared_ptr<const LogTables> log_tables_for(uint64_t N) {
   static std::mutex mu;
@@ -836,6 +870,7 @@ std::shared_ptr<const LogTables> log_tables_for(uint64_t N) {
     gmax = std::max(gmax, std::fabs(g));
   }
   t->kshift = -27.0 * alpha + k2_screen_margin(gmax, double(N), alpha);
+  t->st_c1 = float(-(1.0 + alpha));
   std::lock_guard<std::mutex> g(mu);
   if (cache.size() >= 4) cache.erase(cache.begin());
   cache.emplace_back(N, t);
@@ -995,6 +1030,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
                            cudaMemcpyHostToDevice, ds->stream));
   ds->ktab_n = uint32_t(lt->ktab.size());
   ds->kshift = lt->kshift;
+  ds->st_c1 = lt->st_c1;
   CUDA_TRY(dmalloc(ds, &ds->ktab, sizeof(float) * lt->ktab.size()));
   CUDA_TRY(cudaMemcpyAsync(ds->ktab, lt->ktab.data(), sizeof(float) * lt->ktab.size(),
                            cudaMemcpyHostToDevice, ds->stream));

@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                   pass[h] = n[26] == 0x7fffffffu;  // profiling: derivation only
                 else
                   pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled(n, ktab_s)
-                                                              : k2_screen_packed(n, ktab_s)) <= thr_f);
+                                                              : k2_screen_packed(n, ktab_s, d.st_c1)) <= thr_f);
               }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
