@@ -96,8 +96,8 @@ struct DevData {
   uint32_t n[2];             // class sample counts N0, N1
   const uint4* planes[2];    // [wq][M][2]
   const uint2* single[2];    // [M]: popc(plane0), popc(plane1)
-  const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y); mirrored at
-                             // [y*M+x] unless narrow (then `pairp` holds the mirror)
+  const uint4* pair[2];      // [M*M], x<y: {00, 01, 10, 11} = popc(Xa_x & Xb_y), mirrored at
+                             // [y*M+x]; built lazily for narrow datasets (ensure_wide)
   // narrow (every N_c < 2^16): class-packed u16 counts, word = class0 | class1 << 16
   const uint4* pairp;        // [M*M] {00, 01, 10, 11}, both triangles
   const uint2* singlep;      // [M] {plane 0, plane 1}
@@ -694,6 +694,9 @@ struct e3_dataset {
   uint4* pairp = nullptr;    // narrow class-packed mirrored pair index (every N_c < 2^16)
   uint2* singlep = nullptr;  // narrow class-packed single counts
   bool narrow = false;
+  // narrow datasets build the wide pair index only when a consumer needs it
+  // (e3_tables/e3_scores, the POPC and masked engines): ensure_wide
+  mutable std::mutex wide_mu;
   uint32_t shift = 0;  // narrow: packed counts scaled by 1 << shift (2 when every N_c < 2^14)
   double* logp = nullptr;
   float* ktab = nullptr;              // K2 screening table (see k2_screen)
@@ -885,6 +888,55 @@ struct GenoSrc {
   uint64_t N = 0;
 };
 
+// The pair index launch: narrow_only writes the class-packed mirrored index
+// (what the narrow SYRK engine reads), else the wide per-class index (upper
+// triangle + mirror).
+int launch_pairs(e3_dataset* ds, bool narrow_only) {
+  const uint32_t M = uint32_t(ds->M);
+  pairs_tc::PArgs pa{};
+  pa.M = M;
+  pa.nb = (M + pairs_tc::kBlk - 1) / pairs_tc::kBlk;
+  pa.tiles = uint64_t(pa.nb) * (pa.nb + 1) / 2;
+  pa.pairp = ds->pairp;
+  pa.shift = ds->shift;
+  for (int c = 0; c < 2; ++c) {
+    pa.wq[c] = ds->wq[c];
+    pa.planes[c] = ds->planes[c];
+    pa.pair[c] = ds->pair[c];
+  }
+  CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(pairs_tc::smem_bytes())));
+  CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(pairs_tc::smem_bytes())));
+  const uint32_t grid = uint32_t(std::min<uint64_t>(ds->num_sms, pa.tiles));
+  if (std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 23)) {
+    if (narrow_only)
+      pairs_tc::pairs_tc_kernel<true><<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
+    else
+      pairs_tc::pairs_tc_kernel<false><<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
+  } else {
+    for (int c = 0; c < 2; ++c)
+      pairs_kernel<<<dim3((M + 255) / 256, M), 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
+                                                                   ds->pair[c]);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return E3_OK;
+}
+
+// Builds the wide pair index of a narrow dataset on first use (stream-ordered
+// before the caller's kernels on ds->stream).
+int ensure_wide(const e3_dataset* cds) {
+  e3_dataset* ds = const_cast<e3_dataset*>(cds);
+  std::lock_guard<std::mutex> g(ds->wide_mu);
+  if (ds->pair[0]) return E3_OK;
+  CUDA_TRY(cudaSetDevice(ds->device));
+  for (int c = 0; c < 2; ++c)
+    CUDA_TRY(dmalloc(ds, &ds->pair[c], sizeof(uint4) * size_t(ds->M) * ds->M));
+  return launch_pairs(ds, false);
+}
+
 int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) {
   // E3_TRACE_CREATE=1: per-phase wall times of dataset creation on stderr
   const bool trace = std::getenv("E3_TRACE_CREATE") != nullptr;
@@ -944,7 +996,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
     const uint32_t w64 = uint32_t((n + 63) / 64);
     ds->wq[c] = uint32_t((n + 127) / 128);
     CUDA_TRY(dmalloc(ds, &ds->single[c], sizeof(uint2) * M));
-    CUDA_TRY(dmalloc(ds, &ds->pair[c], sizeof(uint4) * size_t(M) * M));
+    if (!ds->narrow) CUDA_TRY(dmalloc(ds, &ds->pair[c], sizeof(uint4) * size_t(M) * M));
 
     // one extra zero quad: the search kernel steps two quads at a time
     const size_t plane_bytes = sizeof(uint4) * (size_t(ds->wq[c]) + 1) * M * 2;
@@ -982,39 +1034,9 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   dfree(ds, dgeno);
   dfree(ds, didx);
   mark("planes");
-  {
-    // marginal pair index of both classes: one tensor-core Gram launch
-    pairs_tc::PArgs pa{};
-    pa.M = M;
-    pa.nb = (M + pairs_tc::kBlk - 1) / pairs_tc::kBlk;
-    pa.tiles = uint64_t(pa.nb) * (pa.nb + 1) / 2;
-    pa.pairp = ds->pairp;
-    pa.shift = ds->shift;
-    for (int c = 0; c < 2; ++c) {
-      pa.wq[c] = ds->wq[c];
-      pa.planes[c] = ds->planes[c];
-      pa.pair[c] = ds->pair[c];
-
-    }
-    CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(pairs_tc::smem_bytes())));
-    CUDA_TRY(cudaFuncSetAttribute(pairs_tc::pairs_tc_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(pairs_tc::smem_bytes())));
-    const uint32_t grid = uint32_t(std::min<uint64_t>(ds->num_sms, pa.tiles));
-    if (std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 23)) {
-      if (ds->narrow)
-        pairs_tc::pairs_tc_kernel<true><<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
-      else
-        pairs_tc::pairs_tc_kernel<false><<<grid, pairs_tc::kThreadsP, pairs_tc::smem_bytes(), ds->stream>>>(pa);
-    } else {
-      for (int c = 0; c < 2; ++c)
-        pairs_kernel<<<dim3((M + 255) / 256, M), 256, 0, ds->stream>>>(ds->planes[c], M, ds->wq[c],
-                                                                     ds->pair[c]);
-    }
-    CUDA_TRY(cudaGetLastError());
-  }
+  // marginal pair index of both classes: one tensor-core Gram launch (the
+  // class-packed mirrored index only, when narrow)
+  if (int rc = launch_pairs(ds, ds->narrow)) return rc;
   mark("pairs");
   for (int c = 0; c < 2; ++c) {
     ds->h_single[c].resize(M);
@@ -1454,6 +1476,8 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   }
   a.out_lists = ds->lists[0];
   a.out_counts = ds->counts[0];
+  if (!use_syrk)
+    if (int rc = ensure_wide(ds)) return rc;
   const DevData d = dev_view(ds);
   const size_t smem = 2 * sizeof(uint64_t) * kWarps * K;
 
@@ -1550,6 +1574,7 @@ int run_triples(const e3_dataset* ds, const uint32_t* triples, uint64_t n, uint3
   }
   if (n == 0) return E3_OK;
   CUDA_TRY(cudaSetDevice(ds->device));
+  if (int rc = ensure_wide(ds)) return rc;
   uint32_t* d_tri = nullptr;
   uint32_t* d_tab = nullptr;
   double* d_sc = nullptr;

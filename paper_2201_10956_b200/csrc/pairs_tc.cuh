@@ -56,8 +56,9 @@ struct PWalker {
 
 constexpr int kRing = 3;  // TMEM accumulators (128 columns each) + scale factors at kSfCol
 
-// kNarrow: the wide index gets the upper triangle only (what the other
-// engines read) and the SYRK engine's mirrored index is written class-packed.
+// kNarrow: only the SYRK engine's class-packed mirrored index is written (the
+// wide index of a narrow dataset is built by a later <false> launch on first
+// use); else the wide per-class index, upper triangle + mirror.
 template <bool kNarrow>
 __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -179,8 +180,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
     }
   } else {
     // drain both classes of a tile together: lane = row (x, a), columns (y, b)
-    // -> wide uint2 {b=0, b=1} at component offset 2a of pair[c][x*M + y]
-    // (and its mirror unless narrow), narrow class-packed uint2 at offset 2a of
+    // -> wide uint2 {b=0, b=1} at component offset 2a of pair[c][x*M + y] and
+    // its mirror, or (narrow) the class-packed uint2 at offset 2a of
     // pairp[x*M + y] and pairp[y*M + x]
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -212,8 +213,6 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
               const uint2 w1 = e1 ? make_uint2(0u, 0u)
                                   : make_uint2(syrk::f32_count(v1[2 * e]), syrk::f32_count(v1[2 * e + 1]));
               const size_t up = size_t(x) * p.M + y, lo = size_t(y) * p.M + x;
-              *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[0] + up) + 2 * a) = w0;
-              *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[1] + up) + 2 * a) = w1;
               if (kNarrow) {
                 const uint32_t sh = p.shift;
                 const uint2 pk = make_uint2((w0.x << sh) | (w1.x << (16 + sh)),
@@ -221,6 +220,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
                 *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pairp + up) + 2 * a) = pk;
                 *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pairp + lo) + 2 * a) = pk;
               } else {
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[0] + up) + 2 * a) = w0;
+                *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[1] + up) + 2 * a) = w1;
                 *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[0] + lo) + 2 * a) = w0;
                 *reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(p.pair[1] + lo) + 2 * a) = w1;
               }
