@@ -275,3 +275,39 @@ def test_snp_block_edges(engine, M):
     with epi3.DeviceDataset(ds) as dd:
         got = hits_of(dd.search(epi3.SearchConfig(top_k=7, engine=engine)))
     assert_hits_identical(got, po.OracleDataset.of(ds).search(top_k=7))
+
+
+@pytest.mark.parametrize("order", ["search_first", "tables_first", "engines_alternate"])
+def test_lazy_wide_pair_index(order):
+    """A narrow dataset (every class < 2^16) builds only the class-packed pair
+    index at creation; the wide index appears on the first call that reads it
+    (tables/scores, the masked and POPC engines). Every call order gives the
+    oracle's answers on ONE dataset."""
+    ds = _random_ds(40, 700, 333, 41)
+    od = po.OracleDataset.of(ds)
+    P = od.log_table()
+    expect = od.search(top_k=25)
+    triples = [(0, 1, 2), (3, 17, 39), (5, 6, 38), (20, 21, 22)]
+    want_tabs = [od.table(t) for t in triples]
+
+    def check_tables(dd):
+        tabs, scores = dd.tables(triples), dd.scores(triples)
+        for t, tab, w, s in zip(triples, tabs, want_tabs, scores):
+            assert (tab == w).all(), t
+            assert float(s).hex() == po.k2_score(w, P).hex(), t
+
+    def check_search(dd, engine):
+        assert_hits_identical(hits_of(dd.search(epi3.SearchConfig(top_k=25, engine=engine))), expect)
+
+    with epi3.DeviceDataset(ds) as dd:
+        if order == "search_first":
+            check_search(dd, "syrk")
+            check_tables(dd)
+            check_search(dd, "syrk")
+        elif order == "tables_first":
+            check_tables(dd)
+            check_search(dd, "syrk")
+        else:
+            for engine in ["syrk", "tc_masked", "syrk", "popc", "syrk"]:
+                check_search(dd, engine)
+            check_tables(dd)
