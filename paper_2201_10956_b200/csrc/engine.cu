@@ -1330,15 +1330,15 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   const size_t lists_b = size_t(tc::kEpilogueWarps) * 2 * K * sizeof(uint64_t);
   const size_t tab_b = sizeof(float) * ds->ktab_n;
   const size_t cap = ds->smem_optin - 2048;
-  uint32_t nst = syrk::kSStages;
+  uint32_t nst = syrk::kSyrkStages;
   bool screen = !std::getenv("E3_NO_SCREEN");
-  if (const char* e = std::getenv("E3_SYRK_STAGES")) nst = uint32_t(std::max(2, std::min(syrk::kSStages, std::atoi(e))));
+  if (const char* e = std::getenv("E3_SYRK_STAGES")) nst = uint32_t(std::max(2, std::min(syrk::kSyrkStages, std::atoi(e))));
   if (screen) {
-    while (nst > 2 && 1024 + nst * syrk::kSStageBytes + lists_b + tab_b > cap) --nst;
-    screen = 1024 + nst * syrk::kSStageBytes + lists_b + tab_b <= cap;
-    if (!screen) nst = syrk::kSStages;
+    while (nst > 2 && 1024 + nst * syrk::kSBStageBytes + lists_b + tab_b > cap) --nst;
+    screen = 1024 + nst * syrk::kSBStageBytes + lists_b + tab_b <= cap;
+    if (!screen) nst = syrk::kSyrkStages;
   }
-  const size_t tsm = 1024 + nst * syrk::kSStageBytes + lists_b + (screen ? tab_b : 0);
+  const size_t tsm = 1024 + nst * syrk::kSBStageBytes + lists_b + (screen ? tab_b : 0);
   // compaction waits for the metadata upload (and all earlier work on st)
   CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_upload, 0));
   for (size_t b = 0; b < batches.size(); ++b) {

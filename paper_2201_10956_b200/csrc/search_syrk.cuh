@@ -33,9 +33,18 @@ constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows ea
 constexpr int kSChunk = 256;                           // samples per stage
 constexpr int kSRowBytes = kSChunk / 2;                // 128 B per operand row
 constexpr int kSStageBytes = 2 * kRows * kSRowBytes;   // A + B = 32 KiB
-constexpr int kSStages = 4;   // stage slots compiled in; a launch uses s.nst of them
+// SYRK operand stages: A (the j rows) lives in TMEM — tcgen05.mma reads it
+// from there ("[a-tmem]"), so neither the producers' stores nor the tensor
+// core's operand reads of A touch shared memory (measured M128 N128 K64:
+// 83.5 cycles vs 127.6 with both operands in shared memory,
+// tools/mxf4_ts_probe.cu) — and B (the k rows) in shared memory.
+constexpr int kSyrkStages = 3;                          // a launch uses s.nst of them
+constexpr int kSBStageBytes = kRows * kSRowBytes;      // B only = 16 KiB
+constexpr uint32_t kAStageCols = kSRowBytes / 4;       // 32 TMEM columns per A stage
+constexpr uint32_t kACol = 416;                        // A stages: columns [416, 512)
 constexpr int kUnits = 3;          // TMEM ring of (tile, a, c) accumulators, 128 columns each
 constexpr uint32_t kSfCol = 384;   // scale-factor columns (UE8M0 1.0)
+static_assert(kACol >= kSfCol + 32 && kACol + kSyrkStages * kAStageCols <= 512, "TMEM columns");
 constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10)          // A, B = E2M1
                             | (uint32_t(128 >> 3) << 17)      // N = 128
                             | (1u << 23)                      // scale type UE8M0
@@ -52,6 +61,37 @@ __device__ __forceinline__ void mma_f4(uint32_t tmem_d, uint64_t adesc, uint64_t
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}"
       ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdescF4), "r"(accumulate), "r"(tsf));
+}
+// A from TMEM (lane = row, column c = row bytes [4c, 4c+4)), B from shared memory.
+__device__ __forceinline__ void mma_f4_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t tsf, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%5], p;\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(kIdescF4), "r"(accumulate), "r"(tsf));
+}
+// One 128-sample quad of an A row as E2M1 nibbles in TMEM column order: the
+// same 16-byte slabs expand_quad_f4 stores, slab 4h+x -> columns 4(4h+x)..+3.
+__device__ __forceinline__ void expand_quad_regs(uint32_t* out, uint4 q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint32_t v = w[x];
+    out[4 * x + 0] = (v << 1) & 0x22222222u;
+    out[4 * x + 1] = v & 0x22222222u;
+    out[4 * x + 2] = (v >> 1) & 0x22222222u;
+    out[4 * x + 3] = (v >> 2) & 0x22222222u;
+  }
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
@@ -116,7 +156,7 @@ struct SyrkArgs {
   uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no scoring, 2 = no
                                      // operand expansion, 4 = derivation without the screen
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
-  uint32_t nst;                      // operand stages in use (2..kSStages)
+  uint32_t nst;                      // operand stages in use (2..kSyrkStages)
 };
 
 // Y_{i,p} by bit compression: for slot p (phase a) and class c, every
@@ -304,9 +344,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                                              ~uintptr_t(1023));
   uint8_t* stages = smem;
   const uint32_t nst = s.nst;  // operand stages in use (fewer frees room for the K2 table)
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + nst * kSStageBytes);
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + nst * kSBStageBytes);
   float* ktab = reinterpret_cast<float*>(lists + size_t(kEpilogueWarps) * 2 * s.top_k);
-  __shared__ uint64_t full_bar[kSStages], empty_bar[kSStages];
+  __shared__ uint64_t full_bar[kSyrkStages], empty_bar[kSyrkStages];
   __shared__ uint64_t tfull_bar[kUnits], tempty_bar[kUnits];
   __shared__ uint32_t tmem_base_sh;
 
@@ -317,7 +357,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   const uint64_t it1 = s.item_begin + s.item_count * (blockIdx.x + 1) / gridDim.x;
 
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kSStages; ++st) {
+    for (int st = 0; st < kSyrkStages; ++st) {
       mbar_init(&full_bar[st], kSyrkProducerWarps);
       mbar_init(&empty_bar[st], 1);
     }
@@ -381,12 +421,12 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               const uint32_t st = n % nst;
               mbar_wait_spin(&full_bar[st], (n / nst) & 1);
               fence_after();
-              const uint32_t abase = smem_u32(stages + st * kSStageBytes);
-              const uint32_t bbase = abase + kRows * kSRowBytes;
+              const uint32_t acol = tmem + kACol + st * kAStageCols;
+              const uint32_t bbase = smem_u32(stages + st * kSBStageBytes);
 #pragma unroll
               for (int kk = 0; kk < kSRowBytes / 32; ++kk)
-                mma_f4(dcol, f4_desc(abase + kk * 256), f4_desc(bbase + kk * 256), tsf,
-                       (ch != 0 || kk != 0) ? 1u : 0u);
+                mma_f4_ts(dcol, acol + kk * 8, f4_desc(bbase + kk * 256), tsf,
+                          (ch != 0 || kk != 0) ? 1u : 0u);
               mma_commit(&empty_bar[st]);
             }
             mma_commit(&tfull_bar[slot]);
@@ -398,11 +438,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     __syncwarp();
   } else if (warp <= kSyrkProducerWarps) {
     // ===================== producers: compacted bits -> E2M1 nibbles =====================
-    // Each thread owns A row r and B row r; the Y words of the next kAhead
-    // stages are prefetched into registers (L2 latency hidden).
-    const int r = threadIdx.x - 32;             // 0..127
+    // Each thread owns A row r (TMEM lane r: a warp reaches only its own lane
+    // quarter, hence r = 32 (warp & 3) + lane) and B row r (shared memory); the
+    // Y words of the next kAhead stages are prefetched into registers.
+    const int r = (warp & 3) * 32 + lane;       // 0..127
     const uint32_t row_off = (r >> 3) * (kSRowBytes / 16) * 128 + (r & 7) * 16;
-    const uint32_t stage_a = smem_u32(stages) + row_off, stage_b = stage_a + kRows * kSRowBytes;
+    const uint32_t stage_b = smem_u32(stages) + row_off;
+    const uint32_t tmem_a = tmem + (uint32_t((warp & 3) * 32) << 16) + kACol;
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
@@ -442,13 +484,18 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               pb[kAhead - 1][1] = __ldg(Yb + o + R);
             }
             mbar_wait(&empty_bar[st], ph ^ 1);
+            fence_after();  // the MMAs that read this A stage have completed
             if (!(s.debug_skip & 2)) {
-              const uint32_t so = st * kSStageBytes;
-              expand_quad_f4(stage_a + so, 0, a0);
-              expand_quad_f4(stage_a + so, 1, a1);
+              uint32_t av[32];
+              expand_quad_regs(av, a0);
+              expand_quad_regs(av + 16, a1);
+              tmem_st32(tmem_a + st * kAStageCols, av);
+              const uint32_t so = st * kSBStageBytes;
               expand_quad_f4(stage_b + so, 0, b0);
               expand_quad_f4(stage_b + so, 1, b1);
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
+            fence_before();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&full_bar[st]);
