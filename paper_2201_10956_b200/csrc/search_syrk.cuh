@@ -32,7 +32,6 @@ constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows ea
 // accumulation, which is exact for counts < 2^24 (host requires N_c < 2^23).
 constexpr int kSChunk = 256;                           // samples per stage
 constexpr int kSRowBytes = kSChunk / 2;                // 128 B per operand row
-constexpr int kSStageBytes = 2 * kRows * kSRowBytes;   // A + B = 32 KiB
 // SYRK operand stages: A (the j rows) lives in TMEM — tcgen05.mma reads it
 // from there ("[a-tmem]"), so neither the producers' stores nor the tensor
 // core's operand reads of A touch shared memory (measured M128 N128 K64:
