@@ -1100,6 +1100,18 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 1, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 1088)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 1, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 1088)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 2, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 1088)));
+  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(ds->smem_optin - 1088)));
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
   mark("tables");
   uint32_t h_bad = 0;
@@ -1334,11 +1346,26 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   bool screen = !std::getenv("E3_NO_SCREEN");
   if (const char* e = std::getenv("E3_SYRK_STAGES")) nst = uint32_t(std::max(2, std::min(syrk::kSyrkStages, std::atoi(e))));
   if (screen) {
-    while (nst > 2 && 1024 + nst * syrk::kSBStageBytes + lists_b + tab_b > cap) --nst;
-    screen = 1024 + nst * syrk::kSBStageBytes + lists_b + tab_b <= cap;
+    while (nst > 2 && 128 + nst * syrk::kSBStageBytes + lists_b + tab_b > cap) --nst;
+    screen = 128 + nst * syrk::kSBStageBytes + lists_b + tab_b <= cap;
     if (!screen) nst = syrk::kSyrkStages;
   }
-  const size_t tsm = 1024 + nst * syrk::kSBStageBytes + lists_b + (screen ? tab_b : 0);
+  size_t tsm = 128 + nst * syrk::kSBStageBytes + lists_b + (screen ? tab_b : 0);
+  // narrow: the epilogue scratch in shared memory when it fits beside the
+  // table (two B stages suffice; A lives in TMEM)
+  bool sscr = false;
+  if (ds->narrow && !std::getenv("E3_NO_SMEM_SCRATCH")) {
+    const size_t cap_ss = ds->smem_optin - 1088;  // 1 KiB static shared memory (ptxas)
+    for (uint32_t n2 = nst; n2 >= 2 && !sscr; --n2) {
+      const size_t t2 = 128 + n2 * syrk::kSBStageBytes + syrk::kSmemScratchBytes + lists_b +
+                        (screen ? tab_b : 0);
+      if (t2 <= cap_ss) {
+        sscr = true;
+        nst = n2;
+        tsm = t2;
+      }
+    }
+  }
   // compaction waits for the metadata upload (and all earlier work on st)
   CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_upload, 0));
   for (size_t b = 0; b < batches.size(); ++b) {
@@ -1381,7 +1408,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     // checks; the others run the unranged kernel
     const uint64_t b_lo = first_rank(bt.first), b_hi = first_rank(bt.first + bt.n);
     const bool part = ranged && (r0 > b_lo || r1 < b_hi);
-    if (ds->narrow && ds->shift) {
+    if (sscr && ds->shift) {
+      if (part) syrk::search_syrk_kernel<true, 2, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, 2, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    } else if (sscr) {
+      if (part) syrk::search_syrk_kernel<true, 1, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, 1, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    } else if (ds->narrow && ds->shift) {
       if (part) syrk::search_syrk_kernel<true, 2><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
       else syrk::search_syrk_kernel<false, 2><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     } else if (ds->narrow) {

@@ -121,6 +121,7 @@ __device__ __forceinline__ void expand_quad_f4(uint32_t row_saddr, int h, uint4 
 }
 constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
 constexpr int kScratchPerThread = kRounds * 32;  // u32: 8 values x 2 classes x 2 phases per round
+constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-packed, 128 KiB
 // 13 warps: warp 0 issues the MMAs, warps 1-4 expand operands (each thread one
 // A row and one B row), warps 5-12 run the epilogue. With 13 warps no SM
 // sub-partition holds more than 4, so each thread may use 128 registers.
@@ -334,16 +335,22 @@ struct SWalker {
 // kMode: 0 = wide, 1 = narrow, 2 = narrow with counts scaled by 4 (every
 // class < 2^14 samples): a packed word then holds the byte offsets of its two
 // counts in the screening table, which saves the index arithmetic per lookup.
-template <bool kRanged, int kMode>
+// kSS (narrow only): the epilogue's thread-private scratch lives in shared
+// memory (after the B stages) instead of per-CTA global memory.
+template <bool kRanged, int kMode, bool kSS = false>
 __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
   constexpr bool kNarrow = kMode >= 1;
+  static_assert(kNarrow || !kSS, "shared-memory scratch is narrow-only");
   constexpr uint32_t kSh = kMode == 2 ? 2u : 0u;  // count scale shift of packed words
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // no-swizzle K-major operand tiles need 16-byte alignment only
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
   uint8_t* stages = smem;
   const uint32_t nst = s.nst;  // operand stages in use (fewer frees room for the K2 table)
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + nst * kSBStageBytes);
+  uint32_t* const sscr = reinterpret_cast<uint32_t*>(smem + nst * kSBStageBytes);
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + nst * kSBStageBytes +
+                                                (kSS ? kSmemScratchBytes : 0));
   float* ktab = reinterpret_cast<float*>(lists + size_t(kEpilogueWarps) * 2 * s.top_k);
   __shared__ uint64_t full_bar[kSyrkStages], empty_bar[kSyrkStages];
   __shared__ uint64_t tfull_bar[kUnits], tempty_bar[kUnits];
@@ -522,7 +529,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     __syncwarp();
     const int jl = quarter * 16 + (lane >> 1);  // row = 2*j_local + b
     const int bsel = lane & 1;
-    uint32_t* scr = s.scratch + size_t(blockIdx.x) * kScratchPerThread * 256 + et;
+    uint32_t* scr = kSS ? sscr + et : s.scratch + size_t(blockIdx.x) * kScratchPerThread * 256 + et;
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
