@@ -717,6 +717,7 @@ struct e3_dataset {
   uint32_t* scratch = nullptr;
   int num_sms = 0, search_ctas_per_sm = 0, search_min_blocks = 1;
   size_t smem_optin = 0;
+  size_t smem_ss_cap = 0;  // dynamic shared memory ceiling of the shared-scratch SYRK kernels
   uint32_t debug_skip = 0;  // E3_DEBUG_SKIP (profiling experiments only)
   bool no_drop = false;     // E3_SYRK_NO_DROP: always compute phases 0 and 1 (A/B testing)
   // scratch reused across searches
@@ -1100,18 +1101,29 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 1, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 1088)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 1, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 1088)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 2, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 1088)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 1088)));
+  {
+    // the shared-scratch kernels run close to the per-block limit: their
+    // dynamic ceiling is the opt-in limit minus their static shared memory
+    cudaFuncAttributes fa{};
+    size_t st_max = 0;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<false, 1, true>));
+    st_max = std::max(st_max, fa.sharedSizeBytes);
+    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<true, 1, true>));
+    st_max = std::max(st_max, fa.sharedSizeBytes);
+    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<false, 2, true>));
+    st_max = std::max(st_max, fa.sharedSizeBytes);
+    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<true, 2, true>));
+    st_max = std::max(st_max, fa.sharedSizeBytes);
+    ds->smem_ss_cap = ds->smem_optin - st_max;
+    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 1, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
+    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 1, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
+    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 2, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
+    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
+  }
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
   mark("tables");
   uint32_t h_bad = 0;
@@ -1355,7 +1367,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   // table (two B stages suffice; A lives in TMEM)
   bool sscr = false;
   if (ds->narrow && !std::getenv("E3_NO_SMEM_SCRATCH")) {
-    const size_t cap_ss = ds->smem_optin - 1088;  // 1 KiB static shared memory (ptxas)
+    const size_t cap_ss = ds->smem_ss_cap;
     for (uint32_t n2 = nst; n2 >= 2 && !sscr; --n2) {
       const size_t t2 = 128 + n2 * syrk::kSBStageBytes + syrk::kSmemScratchBytes + lists_b +
                         (screen ? tab_b : 0);
