@@ -153,17 +153,26 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
           const uint4* Ya = pl + min(2 * kBlk * wk.xb + r, rmax);
           const uint4* Yb = pl + min(2 * kBlk * wk.yb + r, rmax);
           const uint32_t nq = (p.wq[c] + 1) / 2 * 2;  // zero quad pads an odd count
-          uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
-          if (nq) {
-            a0 = __ldg(Ya); a1 = __ldg(Ya + row);
-            b0 = __ldg(Yb); b1 = __ldg(Yb + row);
-          }
+          // plane quads of the next kAhead stages in flight (L2 latency)
+          constexpr uint32_t kAhead = 2;
+          uint4 pa[kAhead][2], pb[kAhead][2];
+#pragma unroll
+          for (uint32_t x = 0; x < kAhead; ++x)
+            if (2 * x < nq) {
+              pa[x][0] = __ldg(Ya + size_t(2 * x) * row); pa[x][1] = __ldg(Ya + size_t(2 * x + 1) * row);
+              pb[x][0] = __ldg(Yb + size_t(2 * x) * row); pb[x][1] = __ldg(Yb + size_t(2 * x + 1) * row);
+            }
           for (uint32_t q = 0; q < nq; q += 2) {
-            const uint4 ca0 = a0, ca1 = a1, cb0 = b0, cb1 = b1;
-            if (q + 2 < nq) {
-              const size_t o = size_t(q + 2) * row;
-              a0 = __ldg(Ya + o); a1 = __ldg(Ya + o + row);
-              b0 = __ldg(Yb + o); b1 = __ldg(Yb + o + row);
+            const uint4 ca0 = pa[0][0], ca1 = pa[0][1], cb0 = pb[0][0], cb1 = pb[0][1];
+#pragma unroll
+            for (uint32_t x = 0; x + 1 < kAhead; ++x) {
+              pa[x][0] = pa[x + 1][0]; pa[x][1] = pa[x + 1][1];
+              pb[x][0] = pb[x + 1][0]; pb[x][1] = pb[x + 1][1];
+            }
+            if (q + 2 * kAhead < nq) {
+              const size_t o = size_t(q + 2 * kAhead) * row;
+              pa[kAhead - 1][0] = __ldg(Ya + o); pa[kAhead - 1][1] = __ldg(Ya + o + row);
+              pb[kAhead - 1][0] = __ldg(Yb + o); pb[kAhead - 1][1] = __ldg(Yb + o + row);
             }
             mbar_wait(&empty_bar[st], ph ^ 1);
             const uint32_t so = st * kSStageBytes;
