@@ -122,11 +122,16 @@ __device__ __forceinline__ void expand_quad_f4(uint32_t row_saddr, int h, uint4 
 constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
 constexpr int kScratchPerThread = kRounds * 32;  // u32: 8 values x 2 classes x 2 phases per round
 constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-packed, 128 KiB
-// 13 warps: warp 0 issues the MMAs, warps 1-4 expand operands (each thread one
-// A row and one B row), warps 5-12 run the epilogue. With 13 warps no SM
-// sub-partition holds more than 4, so each thread may use 128 registers.
+// 16 warps = four warpgroups: WG0 (warps 0-3) expand operands (thread r owns
+// A row r — TMEM lane r, so each warp writes its own lane quarter — and B row
+// r), WG1-2 (warps 4-11) run the epilogue, WG3 warp 12 issues the MMAs (13-15
+// idle). setmaxnreg moves registers to the epilogue: per SM sub-partition
+// (one warp of WG0 and of WG3, two of WG1-2) 88 + 2 * 184 + 56 = 512 = the
+// 16K-register file / 32 lanes (13 uniform warps were capped at 128 each).
 constexpr int kSyrkProducerWarps = 4;
-constexpr int kSyrkThreads = 32 * (1 + kSyrkProducerWarps + kEpilogueWarps);
+constexpr int kSyrkThreads = 32 * 16;
+constexpr int kRegProducer = 88, kRegEpilogue = 184, kRegMma = 56;
+constexpr int kEpiWarp0 = 4, kMmaWarp = 12;
 
 // Per-i layout of the compacted operands (one record per i of the batch).
 struct IInfo {
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   const uint32_t ktab_s = smem_u32(ktab);
   // Block scale factors = 1.0 (UE8M0 0x7F) in columns [kSfCol, kSfCol+32) of
   // all 128 lanes: one epilogue warp per TMEM lane quarter writes them.
-  if (warp > kSyrkProducerWarps && warp <= kSyrkProducerWarps + 4) {
+  if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
     const uint32_t addr = tmem + (uint32_t((warp & 3) * 32) << 16) + kSfCol;
     const uint32_t one = 0x7F7F7F7Fu;
     asm volatile(
@@ -404,7 +409,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   __syncthreads();
   fence_after();
 
-  if (warp == 0) {
+  if (warp >= kMmaWarp) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegMma));
+  }
+  if (warp == kMmaWarp) {
     // ===================== MMA issuer (one thread) =====================
     // Units (tile, a, c) in order; unit u accumulates into ring slot u % kUnits.
     if (lane == 0 && it0 < it1) {
@@ -442,7 +450,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       }
     }
     __syncwarp();
-  } else if (warp <= kSyrkProducerWarps) {
+  } else if (warp < kSyrkProducerWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProducer));
     // ===================== producers: compacted bits -> E2M1 nibbles =====================
     // Each thread owns A row r (TMEM lane r: a warp reaches only its own lane
     // quarter, hence r = 32 (warp & 3) + lane) and B row r (shared memory); the
@@ -511,9 +520,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         wk.next(s);
       }
     }
-  } else {
+  } else if (warp < kMmaWarp) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpilogue));
     // ===================== epilogue =====================
-    const int ew = warp - 1 - kSyrkProducerWarps;  // 0..7
+    const int ew = warp - kEpiWarp0;            // 0..7
     const int half = ew >> 2;                   // k columns [32*half, 32*half+32)
     const int quarter = warp & 3;               // TMEM lane quarter
     const int et = ew * 32 + lane;              // 0..255 scratch slot
