@@ -317,8 +317,8 @@ def main():
                 # stores, scratch/pair loads) as the busiest unit
                 roof["binding_unit"] = {
                     "unit": "L1TEX LSU data path (l1tex__data_pipe_lsu_wavefronts)",
-                    "pct_of_peak": 70.1, "issue_slots_pct": 56.8, "tensor_pipe_pct": 19.6,
-                    "from": "profiles/r01pf_search_cfg3_raw.csv (ncu --set full, cfg3)"}
+                    "pct_of_peak": 71.8, "issue_slots_pct": 56.2, "tensor_pipe_pct": 19.7,
+                    "from": "profiles/r01wg_search_cfg3_raw.csv (ncu --set full, cfg3)"}
         else:
             peak = nsm * POPC_PER_SM_CLK * f_mhz * 1e6 / 1e12
             achieved = kernel_rate * ALG_POPC_PER_ELEMENT / 1e12
