@@ -9,8 +9,10 @@
  * (include/epi3/common.hpp:36-105). The C++ mirror of the reference API
  * (include/epi3/api.hpp in this repo) is implemented on top of these calls.
  *
- * Threading: calls on distinct datasets are independent; one e3_search per
- * dataset at a time (a dataset owns one CUDA stream).
+ * Threading: calls on distinct datasets are independent and may run
+ * concurrently; calls on one dataset (e3_search, e3_tables, e3_scores) are
+ * serialised by a per-dataset mutex, so a dataset may be shared by host
+ * threads like the reference's (immutable, shareable: SPEC.md:126-127).
  */
 #ifndef EPI3CU_H
 #define EPI3CU_H
@@ -77,12 +79,14 @@ typedef struct {
 
 /* Replaces SearchStats (search.hpp:37-41). */
 typedef struct {
-  uint64_t combinations;   /* triples evaluated == rank_end - rank_begin */
+  uint64_t combinations;   /* triples evaluated, counted on the device triple by triple
+                              (search.cpp:175 `++combos`); the call fails (E3_CUDA) unless
+                              it equals rank_end - rank_begin */
   double elapsed_s;        /* host wall time of the call (SearchStats::elapsed_seconds) */
   double kernel_ms;        /* device time of the contingency+K2 kernel (CUDA events) */
   double total_device_ms;  /* device time of all kernels of the search */
-  uint32_t kernel_launches;
-  uint32_t _pad;
+  uint32_t kernel_launches;       /* all kernels of the search */
+  uint32_t main_kernel_launches;  /* launches of the contingency+K2 kernel (SYRK: one per batch) */
 } e3_stats;
 
 /* ---- dataset load (replaces BitPlaneDataset construction: bitplane.hpp:30-31,

@@ -186,3 +186,54 @@ def ref_run(*args, timeout=3600) -> dict:
     if out.returncode != 0:
         raise RuntimeError(f"epi3_ref {args[0]} failed: {out.stderr.strip()}")
     return json.loads(out.stdout)
+
+
+# --------------------------------------------------------------------------
+# bench.py's CPU legs: the workload's input built with the oracle alone, so
+# the reference arm never loads the product library
+# --------------------------------------------------------------------------
+
+
+class _Plant:
+    def __init__(self, triple, target, p_case_match, p_case_other):
+        self.triple, self.target = triple, target
+        self.p_case_match, self.p_case_other = p_case_match, p_case_other
+
+
+def exact_class_fixup(geno, pheno, plant, exact_cases):
+    """The exact-class-count fix-up of e3_generate_synthetic (include/epi3cu.h):
+    flip surplus labels of samples that do not match the plant first, lowest
+    index first, then matching ones only if that was not enough."""
+    pheno = pheno.copy()
+    match = np.ones(pheno.shape[0], dtype=bool)
+    for s, g in zip(plant.triple, plant.target):
+        match &= geno[s] == g
+    cases = int(pheno.sum())
+    for want_match in (False, True):
+        if cases == exact_cases:
+            break
+        idx = np.nonzero(match == want_match)[0]
+        if cases > exact_cases:
+            cand = idx[pheno[idx] == 1][: cases - exact_cases]
+            pheno[cand] = 0
+            cases -= cand.size
+        else:
+            cand = idx[pheno[idx] == 0][: exact_cases - cases]
+            pheno[cand] = 1
+            cases += cand.size
+    return pheno
+
+
+def workload_sample(path, M, N, n1, maf, seed, plant_triple, p_other, m_sub, p_match=0.9):
+    """Writes the first m_sub SNPs x all N samples of a bench workload (the
+    reference generator + exact class counts, identical to the product's
+    generate_synthetic(..., exact_cases=n1)) as an EPI3 file; returns
+    (path, N0, N1)."""
+    plant = _Plant(tuple(plant_triple), (1, 1, 1), p_match, p_other)
+    geno, pheno = generate_synthetic(M, N, maf, seed, plant)
+    pheno = exact_class_fixup(geno, pheno, plant, n1)
+    n0, n1_, ctrl, cases = binarize(geno[:m_sub], pheno)
+    rc = lib.eo_write_packed(str(path).encode(), m_sub, n0, n1_, _ptr(ctrl), _ptr(cases))
+    if rc != 0:
+        raise OSError(f"eo_write_packed {path} failed")
+    return path, n0, n1_

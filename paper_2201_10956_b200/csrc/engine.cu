@@ -342,11 +342,21 @@ __device__ __forceinline__ void accumulate_class(const uint4* __restrict__ plane
   }
 }
 
+// Exactly-once accounting (the reference's `++combos`, search.cpp:175): every
+// thread counts the triples it evaluated (valid and inside the rank range);
+// one atomic per warp at the end of a launch.
+__device__ __forceinline__ void add_evals(unsigned long long* evals, uint64_t n) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(evals, (unsigned long long)n);
+}
+
 struct SearchArgs {
   uint64_t item_begin, item_count;
   uint64_t rank_begin, rank_end;  // used when ranged
   uint32_t top_k;
   uint64_t* gthr;                 // global score-key threshold
+  unsigned long long* evals;      // triples evaluated (device counter)
   ulonglong2* out_lists;          // [gridDim*kWarps][top_k] (skey, tkey)
   uint32_t* out_counts;           // [gridDim*kWarps]
 };
@@ -393,6 +403,7 @@ search_kernel(const DevData d, const SearchArgs a) {
   uint64_t* ls = smem + size_t(warp) * 2 * K;
   uint64_t* lt = ls + K;
   uint32_t n = 0;
+  uint32_t nevals = 0;
   const uint32_t M = d.M;
 
   uint64_t it = a.item_begin + a.item_count * blockIdx.x / gridDim.x;
@@ -453,6 +464,7 @@ search_kernel(const DevData d, const SearchArgs a) {
         valid = r >= a.rank_begin && r < a.rank_end;
       }
       uint64_t s = ~0ull, t = ~0ull;
+      nevals += valid;
       if (valid) {
         uint32_t n0[27], n1[27];
         derive_cells(T0[q], __ldg(d.pair[0] + size_t(i) * M + jc[q]), pik0,
@@ -483,6 +495,7 @@ search_kernel(const DevData d, const SearchArgs a) {
   const size_t list = size_t(blockIdx.x) * kWarps + warp;
   for (uint32_t e = lane; e < n; e += 32) a.out_lists[list * K + e] = make_ulonglong2(ls[e], lt[e]);
   if (lane == 0) a.out_counts[list] = n;
+  add_evals(a.evals, nevals);
 }
 
 }  // namespace
@@ -697,6 +710,11 @@ struct e3_dataset {
   // narrow datasets build the wide pair index only when a consumer needs it
   // (e3_tables/e3_scores, the POPC and masked engines): ensure_wide
   mutable std::mutex wide_mu;
+  // the search/table workspace below (lists, Y, metadata, scratch, events,
+  // the stream) is per dataset: e3_search / e3_tables / e3_scores on one
+  // dataset serialise on this mutex, so a dataset is safely shareable across
+  // host threads like the reference's
+  std::mutex call_mu;
   uint32_t shift = 0;  // narrow: packed counts scaled by 1 << shift (2 when every N_c < 2^14)
   double* logp = nullptr;
   float* ktab = nullptr;              // K2 screening table (see k2_screen)
@@ -713,7 +731,9 @@ struct e3_dataset {
   size_t y_cap = 0;                   // uint4 elements
   syrk::IInfo* info_buf = nullptr;
   uint64_t* syrk_off = nullptr;
-  size_t info_cap = 0;
+  size_t info_cap = 0;                // IInfo records in info_buf
+  size_t off_cap = 0;                 // u64 entries in syrk_off
+  size_t y_budget = 0;                // E3_SYRK_YBUDGET_KIB (tests: many batches at small M), uint4s
   uint32_t* scratch = nullptr;
   int num_sms = 0, search_ctas_per_sm = 0, search_min_blocks = 1;
   size_t smem_optin = 0;
@@ -726,6 +746,7 @@ struct e3_dataset {
   size_t lists_cap = 0;
   uint32_t counts_cap = 0;
   uint64_t* gthr = nullptr;
+  unsigned long long* evals = nullptr;  // device counter of evaluated triples (per search)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_upload = nullptr;
   // SYRK compaction runs on its own stream, one batch ahead of the search
@@ -766,6 +787,7 @@ void release(e3_dataset* ds) {
   dfree(ds, ds->syrk_off);
   dfree(ds, ds->scratch);
   dfree(ds, ds->gthr);
+  dfree(ds, ds->evals);
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
   if (ds->ev_upload) cudaEventDestroy(ds->ev_upload);
@@ -1083,6 +1105,8 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   ds->smem_optin = size_t(smem_optin);
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
+  if (const char* yb = std::getenv("E3_SYRK_YBUDGET_KIB"))
+    ds->y_budget = std::max<size_t>(1, size_t(std::atoll(yb)) * 1024 / sizeof(uint4));
   CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 0>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(ds->smem_optin - 2048)));
@@ -1125,6 +1149,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
   }
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
+  CUDA_TRY(dmalloc(ds, &ds->evals, sizeof(unsigned long long)));
   mark("tables");
   uint32_t h_bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
@@ -1262,8 +1287,10 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     auto c3 = [](uint64_t n) { return n < 3 ? 0 : n * (n - 1) / 2 * (n - 2) / 3; };
     return c3(M) - c3(M - i);
   };
-  constexpr size_t kYBudget = size_t(3) << 20;   // uint4 elements per batch (48 MiB)
-  constexpr size_t kYMax = size_t(16) << 20;     // hard cap (256 MiB per buffer)
+  // uint4 elements per batch (48 MiB); E3_SYRK_YBUDGET_KIB shrinks it so small
+  // datasets plan many batches (tests of the multi-batch path)
+  const size_t kYBudget = ds->y_budget ? ds->y_budget : size_t(3) << 20;
+  const size_t kYMax = std::max(kYBudget, size_t(16) << 20);  // hard cap (256 MiB per buffer)
   struct Batch {
     uint32_t first, n, rmax, qmax;
     size_t ytot;
@@ -1303,7 +1330,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
       // may grow up to kYMax
       const uint64_t bt_tiles = offs.back();
       if (bt.n > 0 && bt.ytot + ysz > kYBudget &&
-          (bt_tiles >= 2ull * grid || bt.ytot + ysz > kYMax))
+          (bt_tiles >= 2ull * grid || bt.ytot + ysz > kYMax || ds->y_budget))
         break;
       for (int a = 0; a < 2; ++a) {
         inf.y_off[a] = bt.ytot;
@@ -1329,15 +1356,21 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     CUDA_TRY(dmalloc(ds, &ds->y_buf, 2 * sizeof(uint4) * std::max<size_t>(ymax, 1)));
     ds->y_cap = ymax;
   }
-  const size_t info_need = infos.size() + offs.size();
-  if (info_need > ds->info_cap) {
+  // the two metadata buffers are sized independently: a later search may need
+  // more IInfo records and fewer batch offsets, or the reverse
+  if (infos.size() > ds->info_cap) {
     dfree(ds, ds->info_buf);
-    dfree(ds, ds->syrk_off);
     ds->info_buf = nullptr;
+    ds->info_cap = 0;
+    CUDA_TRY(dmalloc(ds, &ds->info_buf, sizeof(syrk::IInfo) * infos.size()));
+    ds->info_cap = infos.size();
+  }
+  if (offs.size() > ds->off_cap) {
+    dfree(ds, ds->syrk_off);
     ds->syrk_off = nullptr;
-    CUDA_TRY(dmalloc(ds, &ds->info_buf, sizeof(syrk::IInfo) * std::max<size_t>(infos.size(), 1)));
-    CUDA_TRY(dmalloc(ds, &ds->syrk_off, sizeof(uint64_t) * std::max<size_t>(offs.size(), 1)));
-    ds->info_cap = info_need;
+    ds->off_cap = 0;
+    CUDA_TRY(dmalloc(ds, &ds->syrk_off, sizeof(uint64_t) * offs.size()));
+    ds->off_cap = offs.size();
   }
   CUDA_TRY(cudaMemcpyAsync(ds->info_buf, infos.data(), sizeof(syrk::IInfo) * infos.size(),
                            cudaMemcpyHostToDevice, st));
@@ -1399,6 +1432,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.itemoff = ds->syrk_off + bt.off_at;
     sa.Y = ybuf;
     sa.scratch = ds->scratch;
+    sa.evals = ds->evals;
     sa.debug_skip = ds->debug_skip;
     sa.screen = screen ? 1u : 0u;
     sa.nst = nst;
@@ -1452,6 +1486,8 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   const auto t_start = std::chrono::steady_clock::now();
   e3_dataset* ds = const_cast<e3_dataset*>(cds);
   if (!ds) return fail(E3_DOMAIN, "null dataset");
+  if (!cfg) return fail(E3_DOMAIN, "null search configuration");
+  std::lock_guard<std::mutex> call_lock(ds->call_mu);
   if (cfg->top_k < 1) return fail(E3_DOMAIN, "top_k must be >= 1");
   if (cfg->top_k > E3_MAX_TOP_K)
     return fail(E3_DOMAIN, "top_k above " + std::to_string(E3_MAX_TOP_K) + " is not supported");
@@ -1476,6 +1512,7 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   a.rank_end = r1;
   a.top_k = cfg->top_k;
   a.gthr = ds->gthr;
+  a.evals = ds->evals;
   const bool ranged = !(r0 == 0 && r1 == total);
 
   const uint32_t K = cfg->top_k;
@@ -1529,16 +1566,19 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   cudaStream_t st = ds->stream;
   CUDA_TRY(cudaEventRecord(ds->ev[0], st));
   CUDA_TRY(cudaMemsetAsync(ds->gthr, 0xff, sizeof(uint64_t), st));
+  CUDA_TRY(cudaMemsetAsync(ds->evals, 0, sizeof(unsigned long long), st));
   CUDA_TRY(cudaEventRecord(ds->ev[1], st));
-  uint32_t launches = 1;
+  uint32_t launches = 1, main_launches = 1;
   if (use_syrk) {
     launches = 0;
     if (int rc = run_syrk(ds, d, r0, r1, K, ranged, t0[0], t1[0], grid, &launches)) return rc;
+    main_launches = launches / 2;  // one compaction + one search kernel per batch
   } else if (use_tc) {
     ta.rank_begin = r0;
     ta.rank_end = r1;
     ta.top_k = K;
     ta.gthr = ds->gthr;
+    ta.evals = ds->evals;
     ta.out_lists = ds->lists[0];
     ta.out_counts = ds->counts[0];
     ta.itemoff = ds->itemoff_tc;
@@ -1575,8 +1615,14 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   CUDA_TRY(cudaMemcpyAsync(h.data(), ds->lists[cur], sizeof(ulonglong2) * K,
                            cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&cnt, ds->counts[cur], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  unsigned long long evaluated = 0;
+  CUDA_TRY(cudaMemcpyAsync(&evaluated, ds->evals, sizeof(evaluated), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(ds->ev[3], st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  // exactly-once check: the kernels count every triple they evaluate
+  if (evaluated != r1 - r0 && !(ds->debug_skip & 1))
+    return fail(E3_CUDA, "exactly-once accounting violated: evaluated " + std::to_string(evaluated) +
+                             " triples of the range's " + std::to_string(r1 - r0));
   cnt = std::min(cnt, K);
   for (uint32_t x = 0; x < cnt; ++x) {
     top[x].score = key_score(h[x].x);
@@ -1588,12 +1634,15 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   *n_top = cnt;
   if (stats) {
     float ms = 0.f;
-    stats->combinations = r1 - r0;
+    // counted on the device, triple by triple (exactly-once accounting); the
+    // caller can compare it with rank_end - rank_begin
+    stats->combinations = evaluated;
     cudaEventElapsedTime(&ms, ds->ev[1], ds->ev[2]);
     stats->kernel_ms = ms;
     cudaEventElapsedTime(&ms, ds->ev[0], ds->ev[3]);
     stats->total_device_ms = ms;
     stats->kernel_launches = launches;
+    stats->main_kernel_launches = main_launches;
     stats->elapsed_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   }
@@ -1618,6 +1667,7 @@ int run_triples(const e3_dataset* ds, const uint32_t* triples, uint64_t n, uint3
                                 std::to_string(ds->M) + " SNPs");
   }
   if (n == 0) return E3_OK;
+  std::lock_guard<std::mutex> call_lock(const_cast<e3_dataset*>(ds)->call_mu);
   CUDA_TRY(cudaSetDevice(ds->device));
   if (int rc = ensure_wide(ds)) return rc;
   uint32_t* d_tri = nullptr;

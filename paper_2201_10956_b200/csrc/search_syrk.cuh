@@ -158,6 +158,7 @@ struct SyrkArgs {
   const uint64_t* itemoff;           // [n_i + 1] tile prefix within the batch
   const uint4* Y;
   uint32_t* scratch;                 // [grid][kRounds * 16][256]
+  unsigned long long* evals;         // triples evaluated (device counter, add_evals)
   uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no scoring, 2 = no
                                      // operand expansion, 4 = derivation without the screen
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
@@ -540,6 +541,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     const int jl = quarter * 16 + (lane >> 1);  // row = 2*j_local + b
     const int bsel = lane & 1;
     uint32_t* scr = kSS ? sscr + et : s.scratch + size_t(blockIdx.x) * kScratchPerThread * 256 + et;
+    uint64_t nevals = 0;
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
@@ -682,6 +684,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 valid[h] = rr >= s.rank_begin && rr < s.rank_end;
               }
             }
+            nevals += uint32_t(valid[0]) + uint32_t(valid[1]);
             uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
             if (valid[0] || valid[1]) {
               uint32_t T[2][8];  // [h][a*4 + b*2 + g], class-packed
@@ -813,6 +816,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 valid[h] = rr >= s.rank_begin && rr < s.rank_end;
               }
             }
+            nevals += uint32_t(valid[0]) + uint32_t(valid[1]);
             uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
             if (valid[0] || valid[1]) {
               uint4 pik[2][2];
@@ -879,6 +883,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     }
     for (uint32_t e = lane; e < nlist; e += 32) s.lists[list * K + e] = make_ulonglong2(ls[e], lt[e]);
     if (lane == 0) s.counts[list] = nlist;
+    add_evals(s.evals, nevals);
   }
   fence_before();
   __syncthreads();

@@ -166,6 +166,7 @@ struct TcArgs {
   ulonglong2* out_lists;   // [grid * kEpilogueWarps][top_k]
   uint32_t* out_counts;
   const uint64_t* itemoff; // [M-1]
+  unsigned long long* evals;  // triples evaluated (device counter, add_evals)
 };
 
 template <bool kRanged>
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
       uint64_t* ls = lists + size_t(ew) * 2 * K;
       uint64_t* lt = ls + K;
       uint32_t nlist = 0;
+      uint32_t nevals = 0;
       const int jl = quarter * 8 + (lane >> 2);      // j_local 0..31
       const int ab = lane & 3;                       // this thread's (a,b) row and k phase
       Walker wk;
@@ -375,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
             valid = r >= a.rank_begin && r < a.rank_end;
           }
           uint64_t sk = ~0ull, tk = ~0ull;
+          nevals += valid;
           if (valid) {
             uint32_t n0[27], n1[27];
             derive_cells(T0, pij0, __ldg(d.pair[0] + size_t(i) * M + kc),
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
       for (uint32_t e = lane; e < nlist; e += 32)
         a.out_lists[list * K + e] = make_ulonglong2(ls[e], lt[e]);
       if (lane == 0) a.out_counts[list] = nlist;
+      add_evals(a.evals, nevals);
     }
   } else if (warp > kProducerWarps) {
     const int ew = warp - 1 - kProducerWarps;

@@ -86,7 +86,7 @@ class e3_search_cfg(C.Structure):
 class e3_stats(C.Structure):
     _fields_ = [("combinations", C.c_uint64), ("elapsed_s", C.c_double),
                 ("kernel_ms", C.c_double), ("total_device_ms", C.c_double),
-                ("kernel_launches", C.c_uint32), ("_pad", C.c_uint32)]
+                ("kernel_launches", C.c_uint32), ("main_kernel_launches", C.c_uint32)]
 
 
 class e3_plant(C.Structure):
@@ -315,6 +315,7 @@ class SearchStats:
     kernel_ms: float = 0.0
     total_device_ms: float = 0.0
     kernel_launches: int = 0
+    main_kernel_launches: int = 0
 
 
 @dataclass
@@ -454,7 +455,7 @@ class DeviceDataset:
         _check(lib.e3_search(self._h, C.byref(c), top, C.byref(n), C.byref(st)))
         hits = _hits_from_array(top, n.value)
         stats = SearchStats(st.combinations, st.elapsed_s, [st.combinations], st.kernel_ms,
-                            st.total_device_ms, st.kernel_launches)
+                            st.total_device_ms, st.kernel_launches, st.main_kernel_launches)
         best = hits[0] if hits else Hit(float("inf"), (0, 0, 0))
         return SearchResult(best, hits, cfg.top_k, stats)
 

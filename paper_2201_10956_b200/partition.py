@@ -23,41 +23,52 @@ def rank_range(M: int, rank: int, world: int) -> tuple:
     return epi3.partition(M, world)[rank]
 
 
-def _pack(hits: Sequence[epi3.Hit], top_k: int, device) -> torch.Tensor:
-    t = torch.full((top_k, 4), float("inf"), dtype=torch.float64)
-    for x, h in enumerate(hits[:top_k]):
+def _pack(local: epi3.SearchResult, top_k: int, device) -> torch.Tensor:
+    """This rank's contribution as ONE f64 tensor [top_k + 1, 4]: rows 0..k-1
+    are the top-k hits (score, i0, i1, i2; +inf marks an empty row), the last
+    row carries the rank's work (triples evaluated, elapsed seconds). Counts
+    below 2^53 and SNP indices are exact in f64."""
+    t = torch.full((top_k + 1, 4), float("inf"), dtype=torch.float64)
+    for x, h in enumerate(local.top[:top_k]):
         t[x, 0] = h.score
         t[x, 1:] = torch.tensor(h.triple, dtype=torch.float64)
+    t[top_k, 0] = float(local.stats.combinations_evaluated)
+    t[top_k, 1] = float(local.stats.elapsed_seconds)
+    t[top_k, 2:] = 0.0
     return t.to(device)
 
 
-def _unpack(t: torch.Tensor) -> list:
-    out = []
-    for row in t.cpu().tolist():
-        if row[0] == float("inf"):
-            continue
-        out.append(epi3.Hit(row[0], (int(row[1]), int(row[2]), int(row[3]))))
-    return out
+def _unpack(t: torch.Tensor, world: int, top_k: int):
+    rows = t.cpu().view(world, top_k + 1, 4).tolist()
+    hits, work, elapsed = [], [], []
+    for r in rows:
+        for row in r[:top_k]:
+            if row[0] == float("inf"):
+                continue
+            hits.append(epi3.Hit(row[0], (int(row[1]), int(row[2]), int(row[3]))))
+        work.append(int(r[top_k][0]))
+        elapsed.append(r[top_k][1])
+    return hits, work, elapsed
 
 
 def allgather_merge(local: epi3.SearchResult, top_k: int, group=None,
                     device=None) -> epi3.SearchResult:
-    """The single collective of a multi-GPU search: all-gather every rank's
-    top-k (k x 32 B) and merge with hit_less + dedup + truncate."""
+    """The single collective of a multi-GPU search: one all-gather of every
+    rank's top-k plus its work count ((k+1) x 32 B per rank), then the
+    reduce_results merge (hit_less + dedup + truncate) on every rank."""
     world = dist.get_world_size(group)
     device = device if device is not None else (
         torch.device("cuda", torch.cuda.current_device())
         if dist.get_backend(group) == "nccl" else torch.device("cpu"))
-    mine = _pack(local.top, top_k, device)
-    gathered = torch.empty((world * top_k, 4), dtype=torch.float64, device=device)
+    mine = _pack(local, top_k, device)
+    gathered = torch.empty((world * (top_k + 1), 4), dtype=torch.float64, device=device)
     dist.all_gather_into_tensor(gathered, mine, group=group)
-    work = torch.tensor([local.stats.combinations_evaluated], dtype=torch.int64, device=device)
-    works = torch.empty(world, dtype=torch.int64, device=device)
-    dist.all_gather_into_tensor(works, work, group=group)
-    merged = epi3.merge_hits(_unpack(gathered), top_k)
+    hits, work, elapsed = _unpack(gathered, world, top_k)
+    merged = epi3.merge_hits(hits, top_k)
     best = merged[0] if merged else epi3.Hit(float("inf"), (0, 0, 0))
-    stats = epi3.SearchStats(int(works.sum().item()), local.stats.elapsed_seconds,
-                             [int(x) for x in works.cpu().tolist()])
+    # reduce_results sums elapsed seconds (search.cpp:108-125); a parallel
+    # search's wall time is the slowest rank's
+    stats = epi3.SearchStats(sum(work), max(elapsed), work)
     return epi3.SearchResult(best, merged, top_k, stats)
 
 

@@ -165,3 +165,22 @@ def test_merge_matches_oracle_merge():
             for _ in range(200)]
     got = epi3.merge_hits([epi3.Hit(s, t) for s, t in hits], 17)
     assert [(h.score, h.triple) for h in got] == po.merge_tops(hits, 17)
+
+
+def test_oracle_built_bench_sample_equals_product_input():
+    """bench.py's CPU legs build the reference's input with the oracle alone
+    (no product library in the reference arm): it must be byte-identical to
+    the product's workload (generator + exact class counts + binarize)."""
+    import hashlib
+    import tempfile
+    import py_oracle as po
+    for M, N, n1, seed, p_other, m in [(256, 1024, 512, 1001, 0.468, 256),
+                                       (600, 4000, 1000, 77, 0.198, 100)]:
+        plant = epi3.PlantSpec((M // 8, M // 2, 7 * M // 8), (1, 1, 1), 0.9, p_other)
+        g, p = epi3.generate_synthetic(M, N, 0.3, seed, plant, exact_cases=n1)
+        with tempfile.TemporaryDirectory() as d:
+            epi3.write_packed(d + "/a.epi3", epi3.binarize(g[:m], p))
+            po.workload_sample(d + "/b.epi3", M, N, n1, 0.3, seed, plant.triple, p_other, m)
+            a = hashlib.sha256(open(d + "/a.epi3", "rb").read()).hexdigest()
+            b = hashlib.sha256(open(d + "/b.epi3", "rb").read()).hexdigest()
+        assert a == b, (M, N)
