@@ -46,6 +46,8 @@ struct IndexError : Error { using Error::Error; };
 struct ParseError : Error { using Error::Error; };
 struct MagicMismatch : Error { using Error::Error; };
 struct TruncatedFile : Error { using Error::Error; };
+struct InfeasibleCache : Error { using Error::Error; };  // common.hpp:97-100
+struct CapExceeded : Error { using Error::Error; };      // common.hpp:102-105
 struct DeviceError : Error { using Error::Error; };  // CUDA/NCCL/OOM: no reference analogue
 
 // ---- raw data (genotype.hpp:14-33) --------------------------------------------
@@ -126,9 +128,47 @@ struct LogSumTable {
 LogSumTable build_log_table(std::size_t n_max);
 double k2_score(const FrequencyTable& ft, const LogSumTable& logs);
 
+// ---- kernel variants and CPU tiling knobs (kernels.hpp:17-67) ------------------------
+// Accepted for source compatibility; all variants give identical results on
+// the reference and the GPU engine ignores them.
+enum class KernelVariant {
+  NaivePhenotype,        // v1
+  ReducedSplit,          // v2
+  Blocked,               // v3
+  BlockedWide,           // v4
+  ThreadPerCombination,  // tpc
+};
+const char* variant_name(KernelVariant v);                 // kernels.cpp:107-116
+KernelVariant variant_from_name(const std::string& name);  // kernels.cpp:118-125, DomainError
+struct CacheSpec {
+  std::size_t l1_bytes = 48 * 1024;
+  std::uint32_t l1_ways = 12;
+  std::uint32_t ft_ways = 7;
+  std::uint32_t block_ways = 4;
+  std::uint32_t count_bytes = 4;
+};
+struct BlockParams {
+  std::uint32_t block_snps = 1;
+  std::uint32_t block_samples = 1;
+  std::uint32_t sched_edge = 256;
+};
+// kernels.cpp:136-169: the same sizing (and InfeasibleCache) as the reference,
+// so reports print the same block=<B_S,B_P>.
+BlockParams derive_block_params(const CacheSpec& cs, std::uint32_t lane_samples);
+struct InstructionModel {
+  std::uint32_t ops_per_element = 0;
+  double relative_memory = 1.0;
+};
+InstructionModel instruction_count_model(KernelVariant v);  // kernels.cpp:127-134
+
 // ---- search (search.hpp:13-89) ----------------------------------------------------------
 struct SearchConfig {
+  KernelVariant variant = KernelVariant::BlockedWide;  // accepted, no effect on the GPU
+  BlockParams block;                                   // validated (search.cpp:133-135)
+  unsigned threads = 1;                                // validated (search.cpp:130)
   std::uint32_t top_k = 10;
+  std::uint64_t chunk = 1;                             // validated (search.cpp:132)
+  int lanes = 8;                                       // accepted, no effect on the GPU
   std::vector<int> devices = {0};   // GPUs; the triple space is split in equal-work ranges
   std::uint64_t rank_begin = 0;     // lexicographic triple-rank range; [0, 0) = all triples
   std::uint64_t rank_end = 0;
@@ -162,6 +202,29 @@ SearchResult run_search(const BitPlaneDataset& ds, const SearchConfig& cfg);
 SearchResult run_search(const GenotypeMatrix& m, const SearchConfig& cfg);
 SearchResult reduce_results(std::span<const SearchResult> partials);
 
+// ---- throughput report (bench.hpp:12-57; bench.cpp:10-107) ------------------------------
+// elements = C(M,3) * N; the minimum over repeats; the same eleven fields.
+struct BenchReport {
+  KernelVariant variant = KernelVariant::BlockedWide;
+  std::uint64_t num_snps = 0;
+  std::uint64_t num_samples = 0;
+  unsigned threads = 1;
+  double elapsed_seconds = 0.0;
+  std::uint64_t elements = 0;
+  double elements_per_second = 0.0;
+  double elements_per_second_per_thread = 0.0;
+  std::uint32_t model_ops_per_element = 0;
+  double model_bytes_per_element = 0.0;
+  double arithmetic_intensity = 0.0;
+  std::vector<double> repeat_seconds;
+};
+inline constexpr double kNaiveBytesPerElement = 9.0 / 8.0;
+BenchReport make_report(KernelVariant variant, std::uint64_t num_snps, std::uint64_t num_samples,
+                        unsigned threads, std::vector<double> repeat_seconds);
+BenchReport measure(const BitPlaneDataset& ds, const SearchConfig& cfg, unsigned repeats);
+enum class ReportFormat { csv, json };
+std::string emit_report(const BenchReport& report, ReportFormat format);
+
 // ---- per-triple tables (kernels.hpp:75) -----------------------------------------------
 FrequencyTable freq_table_reduced(const BitPlaneDataset& ds, Triple t);
 
@@ -174,8 +237,9 @@ class DeviceDataset {
   ~DeviceDataset();
   DeviceDataset(const DeviceDataset&) = delete;
   DeviceDataset& operator=(const DeviceDataset&) = delete;
+  // engine: 0 auto, else E3_ENGINE_POPC / _TC_MASKED / _SYRK (identical results)
   SearchResult search(std::uint32_t top_k, std::uint64_t rank_begin = 0,
-                      std::uint64_t rank_end = 0) const;
+                      std::uint64_t rank_end = 0, int engine = 0) const;
   std::vector<FrequencyTable> tables(std::span<const Triple> triples) const;
   std::vector<double> scores(std::span<const Triple> triples) const;
   std::size_t num_snps() const { return m_; }

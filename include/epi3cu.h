@@ -63,7 +63,10 @@ typedef struct {
   uint64_t rank_end;    /* 0 = C(M,3) */
 } e3_search_cfg;
 
-#define E3_MAX_TOP_K 256u
+/* top_k <= 256 runs one pass (per-warp top-k lists in shared memory); a larger
+ * top_k runs a second, collecting pass below a bound taken from the first
+ * (exact; about twice the search time). */
+#define E3_MAX_TOP_K 1048576u
 /* Engine selection (e3_search_cfg.flags). All engines produce identical
  * results; 0 = auto (E3_ENGINE_SYRK for N >= 4096 samples with every class
  * < 2^23 samples, else E3_ENGINE_TC_MASKED).

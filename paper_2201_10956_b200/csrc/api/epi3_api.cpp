@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <fstream>
 #include <sstream>
+#include <limits>
 #include <thread>
 
 #include "epi3cu.h"
@@ -262,8 +263,9 @@ DeviceDataset::DeviceDataset(const GenotypeMatrix& m, int device) : m_(m.num_snp
 
 DeviceDataset::~DeviceDataset() { e3_dataset_destroy(h_); }
 
-SearchResult DeviceDataset::search(std::uint32_t top_k, std::uint64_t r0, std::uint64_t r1) const {
-  e3_search_cfg cfg{top_k, 0, r0, r1};
+SearchResult DeviceDataset::search(std::uint32_t top_k, std::uint64_t r0, std::uint64_t r1,
+                                   int engine) const {
+  e3_search_cfg cfg{top_k, std::uint32_t(engine), r0, r1};
   std::vector<e3_hit> hits(std::max<std::uint32_t>(1, top_k));
   std::uint32_t n = 0;
   e3_stats st{};
@@ -320,8 +322,14 @@ namespace {
 // triple-rank range; partials merged by reduce_results.
 template <typename Source>
 SearchResult run_search_impl(const Source& src, std::size_t num_snps, const SearchConfig& cfg) {
+  // argument checks in the reference's order and wording (search.cpp:128-135)
   if (num_snps < 3) throw DimensionError("search needs at least 3 SNPs");
+  if (cfg.threads < 1) throw DomainError("threads must be >= 1");
   if (cfg.top_k < 1) throw DomainError("top_k must be >= 1");
+  if (cfg.chunk < 1) throw DomainError("chunk must be >= 1");
+  if (cfg.block.block_snps < 1 || cfg.block.block_samples < 1)
+    throw DomainError("block parameters must be positive");
+  if (cfg.block.sched_edge < 1) throw DomainError("sched edge must be positive");
   if (cfg.devices.empty()) throw DomainError("at least one device is required");
   const auto t0 = std::chrono::steady_clock::now();
   const std::uint64_t total = num_combinations(num_snps, 3);
@@ -368,6 +376,130 @@ SearchResult run_search(const BitPlaneDataset& ds, const SearchConfig& cfg) {
 
 SearchResult run_search(const GenotypeMatrix& m, const SearchConfig& cfg) {
   return run_search_impl(m, m.num_snps, cfg);
+}
+
+// ---- variants, CPU tiling knobs, bench report -------------------------------------
+const char* variant_name(KernelVariant v) {
+  switch (v) {
+    case KernelVariant::NaivePhenotype: return "v1";
+    case KernelVariant::ReducedSplit: return "v2";
+    case KernelVariant::Blocked: return "v3";
+    case KernelVariant::BlockedWide: return "v4";
+    case KernelVariant::ThreadPerCombination: return "tpc";
+  }
+  return "?";
+}
+
+KernelVariant variant_from_name(const std::string& name) {
+  static const std::pair<const char*, KernelVariant> names[] = {
+      {"v1", KernelVariant::NaivePhenotype}, {"v2", KernelVariant::ReducedSplit},
+      {"v3", KernelVariant::Blocked}, {"v4", KernelVariant::BlockedWide},
+      {"tpc", KernelVariant::ThreadPerCombination}};
+  for (const auto& [n, v] : names)
+    if (name == n) return v;
+  throw DomainError("unknown kernel variant '" + name + "'");
+}
+
+InstructionModel instruction_count_model(KernelVariant v) {
+  // the reference's analytic model (kernels.cpp:127-134): 6 ops per combination
+  // per element for v1, 3 NOR + 2 per combination for the reduced forms
+  if (v == KernelVariant::NaivePhenotype) return {27 * 6, 1.0};
+  return {3 + 2 * 27, 2.0 / 3.0};
+}
+
+BlockParams derive_block_params(const CacheSpec& cs, std::uint32_t lane_samples) {
+  if (cs.l1_bytes == 0 || cs.l1_ways == 0 || cs.ft_ways == 0 || cs.block_ways == 0 ||
+      cs.count_bytes == 0)
+    throw DomainError("cache spec fields must be positive");
+  if (cs.ft_ways + cs.block_ways > cs.l1_ways)
+    throw DomainError("frequency-table and block ways exceed the cache ways");
+  if (lane_samples == 0) throw DomainError("lane_samples must be positive");
+  const std::size_t ft_budget = cs.l1_bytes * cs.ft_ways / cs.l1_ways;
+  const std::size_t blk_budget = cs.l1_bytes * cs.block_ways / cs.l1_ways;
+  // largest B_S with B_S^3 tables of 54 cells in the table ways
+  const std::size_t tables = ft_budget / (std::size_t{2} * kNumCombos * cs.count_bytes);
+  std::uint64_t bs = 0;
+  while ((bs + 1) * (bs + 1) * (bs + 1) <= tables) ++bs;
+  if (bs < 1)
+    throw InfeasibleCache("frequency-table budget of " + std::to_string(ft_budget) +
+                          " B cannot hold one table");
+  // B_P: a multiple of lane_samples with B_S * B_P * 2 cells in the block ways
+  const std::uint64_t bp = blk_budget / (bs * 2 * cs.count_bytes) / lane_samples * lane_samples;
+  if (bp < lane_samples)
+    throw InfeasibleCache("block budget of " + std::to_string(blk_budget) +
+                          " B cannot hold one lane of samples");
+  BlockParams p;
+  p.block_snps = std::uint32_t(bs);
+  p.block_samples = std::uint32_t(bp);
+  return p;
+}
+
+BenchReport make_report(KernelVariant variant, std::uint64_t num_snps, std::uint64_t num_samples,
+                        unsigned threads, std::vector<double> repeat_seconds) {
+  if (repeat_seconds.empty()) throw DomainError("need at least one repeat");
+  if (threads == 0) throw DomainError("threads must be >= 1");
+  BenchReport r;
+  r.variant = variant;
+  r.num_snps = num_snps;
+  r.num_samples = num_samples;
+  r.threads = threads;
+  r.repeat_seconds = std::move(repeat_seconds);
+  r.elapsed_seconds = *std::min_element(r.repeat_seconds.begin(), r.repeat_seconds.end());
+  const unsigned __int128 el = (unsigned __int128)num_combinations(num_snps, 3) * num_samples;
+  if (el > std::numeric_limits<std::uint64_t>::max())
+    throw DomainError("element count exceeds 64 bits");
+  r.elements = std::uint64_t(el);
+  r.elements_per_second = double(r.elements) / r.elapsed_seconds;
+  r.elements_per_second_per_thread = r.elements_per_second / threads;
+  const InstructionModel im = instruction_count_model(variant);
+  r.model_ops_per_element = im.ops_per_element;
+  r.model_bytes_per_element = kNaiveBytesPerElement * im.relative_memory;
+  r.arithmetic_intensity = double(im.ops_per_element) / r.model_bytes_per_element;
+  return r;
+}
+
+BenchReport measure(const BitPlaneDataset& ds, const SearchConfig& cfg, unsigned repeats) {
+  if (repeats < 1) throw DomainError("repeats must be >= 1");
+  std::vector<double> secs;
+  SearchResult first;
+  for (unsigned r = 0; r < repeats; ++r) {
+    SearchResult res = run_search(ds, cfg);
+    if (r == 0) first = res;
+    else if (!same_outcome(first, res)) throw Error("search outcome changed between repeats");
+    secs.push_back(res.stats.elapsed_seconds);
+  }
+  return make_report(cfg.variant, ds.num_snps(), ds.num_samples(), cfg.threads, std::move(secs));
+}
+
+namespace {
+std::string g17(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  return b;
+}
+}  // namespace
+
+std::string emit_report(const BenchReport& r, ReportFormat format) {
+  if (format == ReportFormat::csv)
+    return "variant,M,N,threads,elapsed_s,elements,eps,eps_per_thread,model_ops,model_bytes,ai\n" +
+           std::string(variant_name(r.variant)) + ',' + std::to_string(r.num_snps) + ',' +
+           std::to_string(r.num_samples) + ',' + std::to_string(r.threads) + ',' +
+           g17(r.elapsed_seconds) + ',' + std::to_string(r.elements) + ',' +
+           g17(r.elements_per_second) + ',' + g17(r.elements_per_second_per_thread) + ',' +
+           std::to_string(r.model_ops_per_element) + ',' + g17(r.model_bytes_per_element) + ',' +
+           g17(r.arithmetic_intensity) + '\n';
+  std::string rep;
+  for (std::size_t i = 0; i < r.repeat_seconds.size(); ++i)
+    rep += (i ? ",\n    " : "\n    ") + g17(r.repeat_seconds[i]);
+  return "{\n  \"variant\": \"" + std::string(variant_name(r.variant)) + "\",\n  \"M\": " +
+         std::to_string(r.num_snps) + ",\n  \"N\": " + std::to_string(r.num_samples) +
+         ",\n  \"threads\": " + std::to_string(r.threads) + ",\n  \"elapsed_s\": " +
+         g17(r.elapsed_seconds) + ",\n  \"elements\": " + std::to_string(r.elements) +
+         ",\n  \"eps\": " + g17(r.elements_per_second) + ",\n  \"eps_per_thread\": " +
+         g17(r.elements_per_second_per_thread) + ",\n  \"model_ops\": " +
+         std::to_string(r.model_ops_per_element) + ",\n  \"model_bytes\": " +
+         g17(r.model_bytes_per_element) + ",\n  \"ai\": " + g17(r.arithmetic_intensity) +
+         ",\n  \"repeats_s\": [" + rep + (rep.empty() ? "" : "\n  ") + "]\n}\n";
 }
 
 FrequencyTable freq_table_reduced(const BitPlaneDataset& ds, Triple t) {

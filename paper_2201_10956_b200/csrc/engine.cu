@@ -57,6 +57,7 @@ constexpr int kTile = 32;                  // j / k tile edge (one SNP per lane)
 constexpr int kWarps = 8;                  // warps per search CTA
 constexpr int kJPerWarp = kTile / kWarps;  // 4 j's per warp -> 4 triples per lane
 constexpr int kMergeCap = 4096;            // entries per bitonic merge CTA
+constexpr uint32_t kListK = 256;           // per-warp shared-memory top-k list capacity
 constexpr uint32_t kMaxSnps = (1u << 21) - 1;
 
 #define CUDA_TRY(expr)                                                              \
@@ -351,12 +352,24 @@ __device__ __forceinline__ void add_evals(unsigned long long* evals, uint64_t n)
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(evals, (unsigned long long)n);
 }
 
+// Candidate collection for top_k above the shared-memory list capacity (the
+// second pass of a large-k search, e3_search): every evaluated triple whose
+// key is <= the fixed global threshold is appended to buf (warp-aggregated
+// atomics); entries past cap are counted but not stored (the host re-runs
+// with a larger buffer).
+struct Collect {
+  ulonglong2* buf = nullptr;  // nullptr: normal mode (per-warp top-k lists)
+  unsigned int* n = nullptr;
+  uint32_t cap = 0;
+};
+
 struct SearchArgs {
   uint64_t item_begin, item_count;
   uint64_t rank_begin, rank_end;  // used when ranged
   uint32_t top_k;
   uint64_t* gthr;                 // global score-key threshold
   unsigned long long* evals;      // triples evaluated (device counter)
+  Collect col;
   ulonglong2* out_lists;          // [gridDim*kWarps][top_k] (skey, tkey)
   uint32_t* out_counts;           // [gridDim*kWarps]
 };
@@ -392,6 +405,30 @@ __device__ void warp_insert(uint64_t* ls, uint64_t* lt, uint32_t& n, uint32_t K,
     if (n == K && lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(gthr),
                                        (unsigned long long)ls[K - 1]);
   }
+}
+
+// One evaluated triple per lane (valid, score key sk, triple key tk) offered
+// to the warp's sorted top-k list — or, in collect mode, appended to the
+// global candidate buffer when its key passes the fixed threshold.
+__device__ __forceinline__ void offer(bool valid, uint64_t sk, uint64_t tk, uint64_t gth,
+                                      uint64_t* ls, uint64_t* lt, uint32_t& nlist, uint32_t K,
+                                      int lane, uint64_t* gthr, const Collect& col) {
+  if (col.buf) {
+    const bool want = valid && sk <= gth;
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(col.n, unsigned(__popc(m)));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      const unsigned idx = base + unsigned(__popc(m & ((1u << lane) - 1u)));
+      if (want && idx < col.cap) col.buf[idx] = make_ulonglong2(sk, tk);
+    }
+    return;
+  }
+  const bool want = valid && sk <= gth && (nlist < K || key_less(sk, tk, ls[K - 1], lt[K - 1]));
+  const unsigned cand = __ballot_sync(0xffffffffu, want);
+  if (cand) warp_insert(ls, lt, nlist, K, cand, sk, tk, lane, gthr);
 }
 
 template <bool kRanged, int kMinBlocks>
@@ -476,9 +513,7 @@ search_kernel(const DevData d, const SearchArgs a) {
         s = score_key(k2_device(n0, n1, d.logp));
         t = triple_key(i, j[q], k);
       }
-      const bool want = valid && s <= gth && (n < K || key_less(s, t, ls[K - 1], lt[K - 1]));
-      const unsigned cand = __ballot_sync(0xffffffffu, want);
-      if (cand) warp_insert(ls, lt, n, K, cand, s, t, lane, a.gthr);
+      offer(valid, s, t, gth, ls, lt, n, K, lane, a.gthr, a.col);
     }
 
     // advance to the next item in (i, ta, tb) order
@@ -747,6 +782,9 @@ struct e3_dataset {
   uint32_t counts_cap = 0;
   uint64_t* gthr = nullptr;
   unsigned long long* evals = nullptr;  // device counter of evaluated triples (per search)
+  ulonglong2* cand = nullptr;           // large-k candidate buffer (second pass), on first use
+  size_t cand_cap = 0;
+  unsigned int* cand_n = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_upload = nullptr;
   // SYRK compaction runs on its own stream, one batch ahead of the search
@@ -788,6 +826,8 @@ void release(e3_dataset* ds) {
   dfree(ds, ds->scratch);
   dfree(ds, ds->gthr);
   dfree(ds, ds->evals);
+  dfree(ds, ds->cand);
+  dfree(ds, ds->cand_n);
   for (auto& e : ds->ev)
     if (e) cudaEventDestroy(e);
   if (ds->ev_upload) cudaEventDestroy(ds->ev_upload);
@@ -1098,10 +1138,10 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
                            ds->stream));
   CUDA_TRY(cudaFuncSetAttribute(tc::search_tc_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(tc::smem_bytes(E3_MAX_TOP_K))));
+                                int(tc::smem_bytes(kListK))));
   CUDA_TRY(cudaFuncSetAttribute(tc::search_tc_kernel<true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(tc::smem_bytes(E3_MAX_TOP_K))));
+                                int(tc::smem_bytes(kListK))));
   ds->smem_optin = size_t(smem_optin);
   if (const char* dbg = std::getenv("E3_DEBUG_SKIP")) ds->debug_skip = uint32_t(std::atoi(dbg));
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
@@ -1150,6 +1190,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   }
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
   CUDA_TRY(dmalloc(ds, &ds->evals, sizeof(unsigned long long)));
+  CUDA_TRY(dmalloc(ds, &ds->cand_n, sizeof(unsigned int)));
   mark("tables");
   uint32_t h_bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, ds->stream));
@@ -1169,7 +1210,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
                 "set padding bits)");
   CUDA_TRY(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(ulonglong2) * 2 * kMergeCap)));
-  const int list_smem = int(2 * sizeof(uint64_t) * kWarps * E3_MAX_TOP_K);
+  const int list_smem = int(2 * sizeof(uint64_t) * kWarps * kListK);
   CUDA_TRY(cudaFuncSetAttribute(search_kernel<false, 1>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem));
   CUDA_TRY(cudaFuncSetAttribute(search_kernel<true, 1>,
@@ -1279,7 +1320,8 @@ namespace {
 // positions + gather + SYRK kernel; the per-CTA top-k lists persist across
 // the batches. All batches are planned up front, so the host never waits.
 int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_t K, bool ranged,
-             uint32_t i_first, uint32_t i_last, uint32_t grid, uint32_t* launches) {
+             uint32_t i_first, uint32_t i_last, uint32_t grid, uint32_t* launches,
+             const Collect& col) {
   const uint64_t M = ds->M;
   cudaStream_t st = ds->stream;
   // lexicographic rank of the first triple with first SNP i: C(M,3) - C(M-i,3)
@@ -1433,6 +1475,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.Y = ybuf;
     sa.scratch = ds->scratch;
     sa.evals = ds->evals;
+    sa.col = col;
     sa.debug_skip = ds->debug_skip;
     sa.screen = screen ? 1u : 0u;
     sa.nst = nst;
@@ -1510,12 +1553,17 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   a.item_count = ds->h_itemoff[t1[0] + 1] - a.item_begin;
   a.rank_begin = r0;
   a.rank_end = r1;
-  a.top_k = cfg->top_k;
   a.gthr = ds->gthr;
   a.evals = ds->evals;
   const bool ranged = !(r0 == 0 && r1 == total);
 
   const uint32_t K = cfg->top_k;
+  // Per-warp lists hold Kl <= kListK entries in shared memory. A larger k
+  // runs two passes: the union of all lists of a Kl-pass is a set of >= k
+  // distinct scored triples, so its k-th best key bounds the global top-k;
+  // the second pass collects every triple at or below that bound, and the
+  // host sorts the candidates (exact: no top-k triple can exceed the bound).
+  const uint32_t Kl = std::min<uint32_t>(K, kListK);
   // Engines: compacted tensor-core SYRK (default), masked tensor-core GEMM,
   // LOP3/POPC. All produce identical results.
   uint32_t engine = cfg->flags & 3u;
@@ -1543,13 +1591,14 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
     grid = uint32_t(std::max<uint64_t>(1, grid64));
     nlists = grid * kWarps;
   }
-  const size_t need = size_t(nlists) * K;
+  const size_t need = size_t(nlists) * Kl;
   if (need > ds->lists_cap || nlists > ds->counts_cap) {
     for (int b = 0; b < 2; ++b) {
       dfree(ds, ds->lists[b]);
       dfree(ds, ds->counts[b]);
       ds->lists[b] = nullptr;
       ds->counts[b] = nullptr;
+      ds->lists_cap = ds->counts_cap = 0;
       CUDA_TRY(dmalloc(ds, &ds->lists[b], sizeof(ulonglong2) * need));
       CUDA_TRY(dmalloc(ds, &ds->counts[b], sizeof(uint32_t) * nlists));
     }
@@ -1561,69 +1610,152 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   if (!use_syrk)
     if (int rc = ensure_wide(ds)) return rc;
   const DevData d = dev_view(ds);
-  const size_t smem = 2 * sizeof(uint64_t) * kWarps * K;
-
+  const size_t smem = 2 * sizeof(uint64_t) * kWarps * Kl;
   cudaStream_t st = ds->stream;
+
+  // one pass of the selected engine over [r0, r1): per-warp lists of Kl
+  // entries, or (col.buf set) candidate collection below the fixed threshold
+  uint32_t launches = 0, main_launches = 0;
+  auto run_pass = [&](const Collect& col) -> int {
+    CUDA_TRY(cudaMemsetAsync(ds->evals, 0, sizeof(unsigned long long), st));
+    if (use_syrk) {
+      uint32_t l = 0;
+      if (int rc = run_syrk(ds, d, r0, r1, Kl, ranged, t0[0], t1[0], grid, &l, col)) return rc;
+      launches += l;
+      main_launches += l / 2;  // one compaction + one search kernel per batch
+    } else if (use_tc) {
+      ta.rank_begin = r0;
+      ta.rank_end = r1;
+      ta.top_k = Kl;
+      ta.gthr = ds->gthr;
+      ta.evals = ds->evals;
+      ta.col = col;
+      ta.out_lists = ds->lists[0];
+      ta.out_counts = ds->counts[0];
+      ta.itemoff = ds->itemoff_tc;
+      const size_t tsm = tc::smem_bytes(Kl);
+      if (ranged) tc::search_tc_kernel<true><<<grid, tc::kThreads, tsm, st>>>(d, ta);
+      else tc::search_tc_kernel<false><<<grid, tc::kThreads, tsm, st>>>(d, ta);
+      ++launches;
+      ++main_launches;
+    } else {
+      a.top_k = Kl;
+      a.col = col;
+      if (ds->search_min_blocks == 2) {
+        if (ranged) search_kernel<true, 2><<<grid, kWarps * 32, smem, st>>>(d, a);
+        else search_kernel<false, 2><<<grid, kWarps * 32, smem, st>>>(d, a);
+      } else {
+        if (ranged) search_kernel<true, 1><<<grid, kWarps * 32, smem, st>>>(d, a);
+        else search_kernel<false, 1><<<grid, kWarps * 32, smem, st>>>(d, a);
+      }
+      ++launches;
+      ++main_launches;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return E3_OK;
+  };
+  // exactly-once check after each pass: the kernels count every triple they evaluate
+  auto check_evals = [&]() -> int {
+    unsigned long long evaluated = 0;
+    CUDA_TRY(cudaMemcpyAsync(&evaluated, ds->evals, sizeof(evaluated), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (evaluated != r1 - r0 && !(ds->debug_skip & 1))
+      return fail(E3_CUDA, "exactly-once accounting violated: evaluated " +
+                               std::to_string(evaluated) + " triples of the range's " +
+                               std::to_string(r1 - r0));
+    return E3_OK;
+  };
+
   CUDA_TRY(cudaEventRecord(ds->ev[0], st));
   CUDA_TRY(cudaMemsetAsync(ds->gthr, 0xff, sizeof(uint64_t), st));
-  CUDA_TRY(cudaMemsetAsync(ds->evals, 0, sizeof(unsigned long long), st));
   CUDA_TRY(cudaEventRecord(ds->ev[1], st));
-  uint32_t launches = 1, main_launches = 1;
-  if (use_syrk) {
-    launches = 0;
-    if (int rc = run_syrk(ds, d, r0, r1, K, ranged, t0[0], t1[0], grid, &launches)) return rc;
-    main_launches = launches / 2;  // one compaction + one search kernel per batch
-  } else if (use_tc) {
-    ta.rank_begin = r0;
-    ta.rank_end = r1;
-    ta.top_k = K;
-    ta.gthr = ds->gthr;
-    ta.evals = ds->evals;
-    ta.out_lists = ds->lists[0];
-    ta.out_counts = ds->counts[0];
-    ta.itemoff = ds->itemoff_tc;
-    const size_t tsm = tc::smem_bytes(K);
-    if (ranged) tc::search_tc_kernel<true><<<grid, tc::kThreads, tsm, st>>>(d, ta);
-    else tc::search_tc_kernel<false><<<grid, tc::kThreads, tsm, st>>>(d, ta);
-  } else if (ds->search_min_blocks == 2) {
-    if (ranged) search_kernel<true, 2><<<grid, kWarps * 32, smem, st>>>(d, a);
-    else search_kernel<false, 2><<<grid, kWarps * 32, smem, st>>>(d, a);
-  } else {
-    if (ranged) search_kernel<true, 1><<<grid, kWarps * 32, smem, st>>>(d, a);
-    else search_kernel<false, 1><<<grid, kWarps * 32, smem, st>>>(d, a);
-  }
-  CUDA_TRY(cudaGetLastError());
+  if (int rc = run_pass(Collect{})) return rc;
   CUDA_TRY(cudaEventRecord(ds->ev[2], st));
-  // Merge rounds: groups of lists -> one list each, until one list remains.
-  uint32_t nl = nlists;
-  int cur = 0;
-  const uint32_t group = std::max<uint32_t>(2, kMergeCap / K);
-  while (nl > 1) {
-    const uint32_t g = std::min(group, nl);
-    uint32_t P = 1;
-    while (P < g * K) P <<= 1;
-    const uint32_t blocks = (nl + g - 1) / g;
-    merge_kernel<<<blocks, 1024, sizeof(ulonglong2) * P, st>>>(
-        ds->lists[cur], ds->counts[cur], nl, K, g, P, ds->lists[cur ^ 1], ds->counts[cur ^ 1]);
-    CUDA_TRY(cudaGetLastError());
-    ++launches;
-    cur ^= 1;
-    nl = blocks;
-  }
-  std::vector<ulonglong2> h(K);
+  float pass1_kernel_ms = 0.f;
+  std::vector<ulonglong2> h;
   uint32_t cnt = 0;
-  CUDA_TRY(cudaMemcpyAsync(h.data(), ds->lists[cur], sizeof(ulonglong2) * K,
-                           cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&cnt, ds->counts[cur], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  unsigned long long evaluated = 0;
-  CUDA_TRY(cudaMemcpyAsync(&evaluated, ds->evals, sizeof(evaluated), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaEventRecord(ds->ev[3], st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  // exactly-once check: the kernels count every triple they evaluate
-  if (evaluated != r1 - r0 && !(ds->debug_skip & 1))
-    return fail(E3_CUDA, "exactly-once accounting violated: evaluated " + std::to_string(evaluated) +
-                             " triples of the range's " + std::to_string(r1 - r0));
-  cnt = std::min(cnt, K);
+  if (K == Kl) {
+    // Merge rounds: groups of lists -> one list each, until one list remains.
+    uint32_t nl = nlists;
+    int cur = 0;
+    const uint32_t group = std::max<uint32_t>(2, kMergeCap / K);
+    while (nl > 1) {
+      const uint32_t g = std::min(group, nl);
+      uint32_t P = 1;
+      while (P < g * K) P <<= 1;
+      const uint32_t blocks = (nl + g - 1) / g;
+      merge_kernel<<<blocks, 1024, sizeof(ulonglong2) * P, st>>>(
+          ds->lists[cur], ds->counts[cur], nl, K, g, P, ds->lists[cur ^ 1], ds->counts[cur ^ 1]);
+      CUDA_TRY(cudaGetLastError());
+      ++launches;
+      cur ^= 1;
+      nl = blocks;
+    }
+    h.resize(K);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), ds->lists[cur], sizeof(ulonglong2) * K,
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&cnt, ds->counts[cur], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(ds->ev[3], st));
+    if (int rc = check_evals()) return rc;
+    cnt = std::min(cnt, K);
+  } else {
+    // ---- large k, pass 1 -> bound: the k-th best key over the union of all lists
+    std::vector<ulonglong2> lists(size_t(nlists) * Kl);
+    std::vector<uint32_t> counts(nlists);
+    CUDA_TRY(cudaMemcpyAsync(lists.data(), ds->lists[0], sizeof(ulonglong2) * lists.size(),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(counts.data(), ds->counts[0], sizeof(uint32_t) * nlists,
+                             cudaMemcpyDeviceToHost, st));
+    if (int rc = check_evals()) return rc;
+    cudaEventElapsedTime(&pass1_kernel_ms, ds->ev[1], ds->ev[2]);
+    std::vector<ulonglong2> uni;
+    for (uint32_t l = 0; l < nlists; ++l)
+      uni.insert(uni.end(), lists.begin() + size_t(l) * Kl,
+                 lists.begin() + size_t(l) * Kl + std::min(counts[l], Kl));
+    auto less = [](const ulonglong2& x, const ulonglong2& y) {
+      return x.x < y.x || (x.x == y.x && x.y < y.y);
+    };
+    uint64_t thr = ~0ull;  // fewer than k triples scored so far: collect everything
+    if (uni.size() >= K) {
+      std::nth_element(uni.begin(), uni.begin() + (K - 1), uni.end(), less);
+      thr = uni[K - 1].x;
+    } else if (r1 - r0 > (uint64_t(1) << 28)) {
+      return fail(E3_DOMAIN, "top_k " + std::to_string(K) + " exceeds what this search can rank");
+    }
+    // ---- pass 2: collect every triple with score key <= thr
+    size_t cap = thr == ~0ull ? size_t(r1 - r0) : std::max<size_t>(size_t(4) * K, size_t(1) << 16);
+    uint32_t n_cand = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (cap > ds->cand_cap) {
+        dfree(ds, ds->cand);
+        ds->cand = nullptr;
+        ds->cand_cap = 0;
+        CUDA_TRY(dmalloc(ds, &ds->cand, sizeof(ulonglong2) * cap));
+        ds->cand_cap = cap;
+      }
+      Collect col;
+      col.buf = ds->cand;
+      col.n = ds->cand_n;
+      col.cap = uint32_t(std::min<size_t>(ds->cand_cap, 0xffffffffu));
+      CUDA_TRY(cudaMemsetAsync(ds->cand_n, 0, sizeof(unsigned int), st));
+      CUDA_TRY(cudaMemcpyAsync(ds->gthr, &thr, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaEventRecord(ds->ev[1], st));
+      if (int rc = run_pass(col)) return rc;
+      CUDA_TRY(cudaEventRecord(ds->ev[2], st));
+      CUDA_TRY(cudaMemcpyAsync(&n_cand, ds->cand_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+      if (int rc = check_evals()) return rc;
+      if (n_cand <= col.cap) break;
+      cap = n_cand;  // the count is exact: a second attempt always fits
+    }
+    h.resize(n_cand);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), ds->cand, sizeof(ulonglong2) * n_cand,
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(ds->ev[3], st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const size_t keep = std::min<size_t>(K, h.size());
+    std::partial_sort(h.begin(), h.begin() + keep, h.end(), less);
+    cnt = uint32_t(keep);
+  }
   for (uint32_t x = 0; x < cnt; ++x) {
     top[x].score = key_score(h[x].x);
     top[x].i0 = uint32_t(h[x].y >> 42);
@@ -1634,11 +1766,11 @@ extern "C" int e3_search(const e3_dataset* cds, const e3_search_cfg* cfg, e3_hit
   *n_top = cnt;
   if (stats) {
     float ms = 0.f;
-    // counted on the device, triple by triple (exactly-once accounting); the
-    // caller can compare it with rank_end - rank_begin
-    stats->combinations = evaluated;
+    // counted on the device, triple by triple (exactly-once accounting,
+    // checked above against rank_end - rank_begin)
+    stats->combinations = r1 - r0;
     cudaEventElapsedTime(&ms, ds->ev[1], ds->ev[2]);
-    stats->kernel_ms = ms;
+    stats->kernel_ms = ms + pass1_kernel_ms;
     cudaEventElapsedTime(&ms, ds->ev[0], ds->ev[3]);
     stats->total_device_ms = ms;
     stats->kernel_launches = launches;

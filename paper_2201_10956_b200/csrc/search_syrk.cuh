@@ -159,6 +159,7 @@ struct SyrkArgs {
   const uint4* Y;
   uint32_t* scratch;                 // [grid][kRounds * 16][256]
   unsigned long long* evals;         // triples evaluated (device counter, add_evals)
+  Collect col;                       // large top_k, second pass (offer)
   uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no scoring, 2 = no
                                      // operand expansion, 4 = derivation without the screen
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
@@ -738,10 +739,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const bool want = valid[h] && sk[h] <= gth &&
-                                (nlist < K || key_less(sk[h], tk[h], ls[K - 1], lt[K - 1]));
-              const unsigned cand = __ballot_sync(0xffffffffu, want);
-              if (cand) warp_insert(ls, lt, nlist, K, cand, sk[h], tk[h], lane, s.gthr);
+              offer(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col);
             }
           }
         } else {
@@ -871,10 +869,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             }
   #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const bool want = valid[h] && sk[h] <= gth &&
-                                (nlist < K || key_less(sk[h], tk[h], ls[K - 1], lt[K - 1]));
-              const unsigned cand = __ballot_sync(0xffffffffu, want);
-              if (cand) warp_insert(ls, lt, nlist, K, cand, sk[h], tk[h], lane, s.gthr);
+              offer(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col);
             }
           }
         }

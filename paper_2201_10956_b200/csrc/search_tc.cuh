@@ -167,6 +167,7 @@ struct TcArgs {
   uint32_t* out_counts;
   const uint64_t* itemoff; // [M-1]
   unsigned long long* evals;  // triples evaluated (device counter, add_evals)
+  Collect col;               // large top_k, second pass (offer)
 };
 
 template <bool kRanged>
@@ -389,10 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) search_tc_kernel(const DevData d,
             sk = score_key(k2_device(n0, n1, d.logp));
             tk = triple_key(i, j, k);
           }
-          const bool want = valid && sk <= gth &&
-                            (nlist < K || key_less(sk, tk, ls[K - 1], lt[K - 1]));
-          const unsigned cand = __ballot_sync(0xffffffffu, want);
-          if (cand) warp_insert(ls, lt, nlist, K, cand, sk, tk, lane, a.gthr);
+          offer(valid, sk, tk, gth, ls, lt, nlist, K, lane, a.gthr, a.col);
         }
         fence_before();
         mbar_arrive(&tempty_bar[buf]);

@@ -95,7 +95,7 @@ class e3_plant(C.Structure):
                 ("p_case_match", C.c_double), ("p_case_other", C.c_double)]
 
 
-MAX_TOP_K = 256
+MAX_TOP_K = 1048576  # E3_MAX_TOP_K; above 256 a search runs two passes
 # e3_search_cfg.flags: 0 = auto, E3_ENGINE_POPC = 1, E3_ENGINE_TC_MASKED = 2,
 # E3_ENGINE_SYRK = 3
 ENGINES = {"auto": 0, "popc": 1, "tc_masked": 2, "syrk": 3}
