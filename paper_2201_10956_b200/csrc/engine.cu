@@ -995,6 +995,15 @@ int ensure_wide(const e3_dataset* cds) {
   std::lock_guard<std::mutex> g(ds->wide_mu);
   if (ds->pair[0]) return E3_OK;
   CUDA_TRY(cudaSetDevice(ds->device));
+  {
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const double need = 32.0 * double(ds->M) * double(ds->M);
+    if (need > double(free_b))
+      return fail(E3_OOM, "the per-class pair index of " + std::to_string(ds->M) + " SNPs needs " +
+                              std::to_string(need / 1e9) + " GB of device memory, " +
+                              std::to_string(double(free_b) / 1e9) + " GB free");
+  }
   for (int c = 0; c < 2; ++c)
     CUDA_TRY(dmalloc(ds, &ds->pair[c], sizeof(uint4) * size_t(ds->M) * ds->M));
   return launch_pairs(ds, false);
@@ -1038,6 +1047,27 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   ds->narrow = std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 16) && !std::getenv("E3_NO_NARROW");
   ds->shift = ds->narrow && std::max(ds->N[0], ds->N[1]) < (uint64_t(1) << 14) &&
                       !std::getenv("E3_NO_SCALED") ? 2u : 0u;
+  {
+    // the marginal pair index is O(M^2) (16 B per SNP pair and class-packed
+    // index, 32 B when wide): refuse up front, with the numbers, what cannot fit
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const double pairs = double(M) * double(M);
+    double need = pairs * (ds->narrow ? 16.0 : 32.0);
+    for (int c = 0; c < 2; ++c) need += 32.0 * (double((ds->N[c] + 127) / 128) + 1.0) * M * 2.0;
+    if (need > double(free_b)) {  // blocks cached by the stream-ordered pool count as used
+      cudaMemPool_t pool;
+      CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, ds->device));
+      CUDA_TRY(cudaDeviceSynchronize());
+      CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
+      CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    }
+    if (need > double(free_b))
+      return fail(E3_OOM, "dataset of " + std::to_string(M) + " SNPs needs " +
+                              std::to_string(need / 1e9) + " GB of device memory (pair index " +
+                              std::to_string(ds->narrow ? 16 : 32) + " B x M^2), " +
+                              std::to_string(double(free_b) / 1e9) + " GB free");
+  }
   uint32_t* bad = nullptr;
   CUDA_TRY(dmalloc(ds, &bad, sizeof(uint32_t)));
   CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), ds->stream));

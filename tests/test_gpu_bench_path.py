@@ -153,3 +153,44 @@ def test_concurrent_searches_on_one_dataset():
         for t in threads:
             t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("engine", ["syrk", "tc_masked", "popc"])
+@pytest.mark.parametrize("M,top_k,ranged", [(40, 300, False), (40, 9880, False), (110, 3000, False),
+                                            (110, 1500, True)])
+def test_top_k_beyond_list_capacity_vs_oracle(engine, M, top_k, ranged):
+    """top_k above the 256-entry shared-memory lists (the reference's top_k is
+    any u32, search.hpp:17): two passes, identical to the oracle's top-k —
+    including k = C(40,3) (every triple ranked)."""
+    ds = _random_ds(M, 400, 380, 64 + M)
+    od = po.OracleDataset.of(ds)
+    total = epi3.num_combinations(M, 3)
+    a, b = (total // 5, total - total // 7) if ranged else (0, total)
+    with epi3.DeviceDataset(ds) as dd:
+        res = dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b, engine=engine))
+    assert res.stats.combinations_evaluated == b - a
+    expect = od.search(top_k=top_k, r0=a, r1=b)
+    assert len(expect) == min(top_k, b - a)
+    assert_hits_identical(hits_of(res), expect)
+
+
+def test_large_m_fits_or_fails_cleanly():
+    """The paper's largest shape (40,000 SNPs) fits one
+    B200 (class-packed pair index 16 B x M^2 = 25.6 GB): a ranged search
+    around the planted triple matches the oracle. A dataset whose pair index
+    cannot fit is refused up front with E3_OOM and a message, not a crash."""
+    M, N = 40000, 6400
+    plant = epi3.PlantSpec((5000, 20000, 35000), (1, 1, 1), 0.9, 0.468)
+    geno, pheno = epi3.generate_synthetic(M, N, 0.3, 7, plant, exact_cases=N // 2)
+    ds = epi3.binarize(geno, pheno)
+    del geno
+    od = po.OracleDataset.of(ds)
+    r_pl = epi3.triple_rank(M, plant.triple)
+    with epi3.DeviceDataset(ds) as dd:
+        res = dd.search(epi3.SearchConfig(top_k=5, rank_begin=r_pl - 50_000, rank_end=r_pl + 50_000))
+        assert_hits_identical(hits_of(res), od.search(top_k=5, r0=r_pl - 50_000, r1=r_pl + 50_000))
+        assert res.best.triple == plant.triple
+    big = epi3.BitPlaneDataset(150_000, 64, 64, np.zeros((150_000, 2, 1), dtype=np.uint64),
+                               np.zeros((150_000, 2, 1), dtype=np.uint64))
+    with pytest.raises(epi3.DeviceError, match="needs .* GB of device memory"):
+        epi3.DeviceDataset(big)
