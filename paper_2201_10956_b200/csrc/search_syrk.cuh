@@ -395,6 +395,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t ktab_s = smem_u32(ktab);
+  // shared addresses of the barriers, hoisted out of the hot loops
+  const uint32_t full_s = smem_u32(full_bar), empty_s = smem_u32(empty_bar);
+  const uint32_t tfull_s = smem_u32(tfull_bar), tempty_s = smem_u32(tempty_bar);
   // Block scale factors = 1.0 (UE8M0 0x7F) in columns [kSfCol, kSfCol+32) of
   // all 128 lanes: one epilogue warp per TMEM lane quarter writes them.
   if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
@@ -429,13 +432,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
           for (uint32_t c = 0; c < 2; ++c, ++u) {
             const uint32_t slot = u % kUnits;
-            mbar_wait(&tempty_bar[slot], ((u / kUnits) & 1) ^ 1);
+            mbar_wait_a(tempty_s + 8 * slot, ((u / kUnits) & 1) ^ 1);
             fence_after();
             const uint32_t nch = inf.q[a][c] / 2;
             const uint32_t dcol = tmem + slot * 128;
             for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
               const uint32_t st = n % nst;
-              mbar_wait_spin(&full_bar[st], (n / nst) & 1);
+              mbar_wait_spin_a(full_s + 8 * st, (n / nst) & 1);
               fence_after();
               const uint32_t acol = tmem + kACol + st * kAStageCols;
               const uint32_t bbase = smem_u32(stages + st * kSBStageBytes);
@@ -443,9 +446,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               for (int kk = 0; kk < kSRowBytes / 32; ++kk)
                 mma_f4_ts(dcol, acol + kk * 8, f4_desc(bbase + kk * 256), tsf,
                           (ch != 0 || kk != 0) ? 1u : 0u);
-              mma_commit(&empty_bar[st]);
+              mma_commit_a(empty_s + 8 * st);
             }
-            mma_commit(&tfull_bar[slot]);
+            mma_commit_a(tfull_s + 8 * slot);
           }
         }
         wk.next(s);
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               pb[kAhead - 1][0] = __ldg(Yb + o);
               pb[kAhead - 1][1] = __ldg(Yb + o + R);
             }
-            mbar_wait(&empty_bar[st], ph ^ 1);
+            mbar_wait_a(empty_s + 8 * st, ph ^ 1);
             fence_after();  // the MMAs that read this A stage have completed
             if (!(s.debug_skip & 2)) {
               uint32_t av[32];
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             fence_before();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&full_bar[st]);
+            if (lane == 0) mbar_arrive_a(full_s + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1; }
           }
         }
@@ -542,6 +545,17 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     const int jl = quarter * 16 + (lane >> 1);  // row = 2*j_local + b
     const int bsel = lane & 1;
     uint32_t* scr = kSS ? sscr + et : s.scratch + size_t(blockIdx.x) * kScratchPerThread * 256 + et;
+    // narrow scratch word x of this thread (x-major, thread-minor): explicit
+    // shared-memory accesses when it lives there (no generic LD/ST)
+    const uint32_t scr_s = kSS ? smem_u32(sscr + et) : 0u;
+    auto scr_st = [&](uint32_t x, uint32_t v) {
+      if constexpr (kSS) sts_u32(scr_s + x * 1024u, v);
+      else scr[x * 256] = v;
+    };
+    auto scr_ld = [&](uint32_t x) -> uint32_t {
+      if constexpr (kSS) return lds_u32(scr_s + x * 1024u);
+      else return scr[x * 256];
+    };
     uint64_t nevals = 0;
     if (it0 < it1) {
       SWalker wk;
@@ -559,8 +573,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
           for (uint32_t a = 0; a < 2; ++a, u += 2) {
             const uint32_t s0 = u % kUnits, s1 = (u + 1) % kUnits;
-            mbar_wait(&tfull_bar[s0], (u / kUnits) & 1);
-            mbar_wait(&tfull_bar[s1], ((u + 1) / kUnits) & 1);
+            mbar_wait_a(tfull_s + 8 * s0, (u / kUnits) & 1);
+            mbar_wait_a(tfull_s + 8 * s1, ((u + 1) / kUnits) & 1);
             fence_after();
             // count c (f32, exact) -> 2^23 + c * 2^kSh by one FFMA (c * 2^kSh < 2^16),
             // then one PRMT joins the low halves of both classes; a class with
@@ -579,12 +593,12 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 const int m = m2 + (x >> 3), tg = x & 7;
                 const uint32_t b0 = e0 ? 0x4B000000u : __float_as_uint(__fmaf_rn(__uint_as_float(v0[x]), scl, 8388608.f));
                 const uint32_t b1 = e1 ? 0x4B000000u : __float_as_uint(__fmaf_rn(__uint_as_float(v1[x]), scl, 8388608.f));
-                scr[(a * kRounds * 8 + m * 8 + tg) * 256] = __byte_perm(b0, b1, 0x5410);
+                scr_st(a * kRounds * 8 + m * 8 + tg, __byte_perm(b0, b1, 0x5410));
               }
             }
             fence_before();
-            mbar_arrive(&tempty_bar[s0]);
-            mbar_arrive(&tempty_bar[s1]);
+            mbar_arrive_a(tempty_s + 8 * s0);
+            mbar_arrive_a(tempty_s + 8 * s1);
           }
         } else {
 #pragma unroll
@@ -610,7 +624,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               }
             }
             fence_before();
-            mbar_arrive(&tempty_bar[slot]);
+            mbar_arrive_a(tempty_s + 8 * slot);
           }
         }
         const uint32_t j = i + 1 + wk.jb * kJB + jl;
@@ -649,7 +663,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               for (int t = 0; t < 4; ++t)
 #pragma unroll
                 for (int g = 0; g < 2; ++g)
-                  Wn[a][t][g] = scr[(a * kRounds * 8 + mm * 8 + t * 2 + g) * 256];
+                  Wn[a][t][g] = scr_ld(a * kRounds * 8 + mm * 8 + t * 2 + g);
           };
           fetch_round(0);
           for (int m = 0; m < kRounds; ++m) {
@@ -716,11 +730,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               for (int h = 0; h < 2; ++h) {
                 uint32_t n[27];
                 derive_cells(T[h], pij, pik[h], pjk[h], sip, sjp, skp[h], d.npk, n);
+                if (s.debug_skip & 2) {  // profiling: operands not expanded -> keep lookups in range
+#pragma unroll
+                  for (int c = 0; c < 27; ++c) n[c] &= 0x0ffc0ffcu;
+                }
                 if (s.debug_skip & 4)
                   pass[h] = n[26] == 0x7fffffffu;  // profiling: derivation only
                 else
                   pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled(n, ktab_s)
-                                                              : k2_screen_packed(n, ktab_s, d.st_c1)) <= thr_f);
+                                                              : k2_screen_packed(n, ktab_s, d.st_c1)) <= thr_f) &&
+                            !(s.debug_skip & 2);
               }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {

@@ -75,7 +75,7 @@ def test_cli_detect_text_input_binarizes_on_device():
         t, p = Path(d) / "g.txt", Path(d) / "g.epi3"
         for out, fmt in ((t, "text"), (p, "packed")):
             subprocess.run([str(build.CLI), "generate", "--snps", "40", "--samples", "900",
-                            "--seed", "9", "--plant", "4,17,31", "--format", fmt, "--out", str(out)],
+                            "--seed", "9", "--plant", "4,17,31:1,1,1:0.9,0.1", "--format", fmt, "--out", str(out)],
                            check=True, capture_output=True)
         rt = json.loads(subprocess.run([str(build.CLI), "detect", "--in", str(t), "--json"],
                                        capture_output=True, text=True, check=True).stdout)

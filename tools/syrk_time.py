@@ -22,10 +22,24 @@ ap.add_argument("--hi", type=float, default=0.375)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--engine", default="auto")
 ap.add_argument("--tag", default="")
+ap.add_argument("--slices", type=int, default=0,
+                help="instead: time each of S equal-triple slices of the full space (cost profile)")
 args = ap.parse_args()
 ds, top_k, planted = bench.make_dataset(args.workload)
 M, N = ds.num_snps, ds.num_samples
 total = epi3.num_combinations(M, 3)
+if args.slices:
+    import json
+    with epi3.DeviceDataset(ds) as dd:
+        out = []
+        for a, b in epi3.partition(M, args.slices):
+            cfg = epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b, engine=args.engine)
+            dd.search(cfg)
+            r = min((dd.search(cfg) for _ in range(args.reps)), key=lambda r: r.stats.kernel_ms)
+            out.append({"a": a, "b": b, "ms": r.stats.kernel_ms, "total_ms": r.stats.total_device_ms,
+                        "batches": r.stats.main_kernel_launches})
+    print(json.dumps({"workload": args.workload, "M": M, "N": N, "slices": out}))
+    sys.exit(0)
 a, b = int(total * args.lo), int(total * args.hi)
 cfg = epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b, engine=args.engine)
 with epi3.DeviceDataset(ds) as dd:
