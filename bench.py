@@ -277,8 +277,9 @@ def main():
                          "tcgen05 kind::mxf4 SYRK; tc_masked: tcgen05 GEMM over pair products; "
                          "popc: LOP3/POPC kernel")
     ap.add_argument("--balance-parts", type=int, default=8,
-                    help="N=1 only: after the timed region, time the P equal-work ranges of "
-                         "one search separately (max/mean bounds P-GPU efficiency); 0 = off")
+                    help="N=1 only: after the timed region, time the P ranges of the P-GPU "
+                         "split (e3_partition_balanced) one by one (max/mean bounds the P-GPU "
+                         "efficiency); 0 = off")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -319,7 +320,7 @@ def main():
     ds, top_k, planted = make_dataset(args.workload)
     M, N = ds.num_snps, ds.num_samples
     total = epi3.num_combinations(M, 3)
-    my_a, my_b = epi3.partition(M, world)[rank]
+    my_a, my_b = epi3.partition_balanced(M, world)[rank]
     cfg = epi3.SearchConfig(top_k=top_k, rank_begin=my_a, rank_end=my_b, engine=args.engine)
     l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
@@ -363,7 +364,7 @@ def main():
     balance = None
     if world == 1 and args.balance_parts > 1:
         times = []
-        for a, b in epi3.partition(M, args.balance_parts):
+        for a, b in epi3.partition_balanced(M, args.balance_parts):
             l2_flush.zero_()
             torch.cuda.synchronize()
             times.append(dd.search(epi3.SearchConfig(top_k=top_k, rank_begin=a, rank_end=b,

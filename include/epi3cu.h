@@ -136,6 +136,10 @@ int e3_triple_unrank(uint64_t M, uint64_t rank, uint32_t* triple3);
 /* Equal-work partition of [0, C(M,3)) into `parts` contiguous rank ranges
  * (the multi-GPU partitioner): bounds has parts+1 entries. */
 int e3_partition(uint64_t M, uint32_t parts, uint64_t* bounds);
+/* The same split balanced by measured device cost instead of triple count
+ * (SYRK engine: a cost per 64x64 (j,k) tile plus a per-first-SNP cost): the
+ * ranges the multi-GPU search uses (bench.py, run_search over devices). */
+int e3_partition_balanced(uint64_t M, uint32_t parts, uint64_t* bounds);
 /* build_log_table (scoring.cpp:14-21): prefix has n_max+1 doubles. */
 int e3_build_log_table(uint64_t n_max, double* prefix);
 /* k2_score (scoring.cpp:23-35) on the host, same grouping and order. */

@@ -337,11 +337,19 @@ SearchResult run_search_impl(const Source& src, std::size_t num_snps, const Sear
   const std::uint64_t r1 = cfg.rank_end == 0 ? total : cfg.rank_end;
   if (r1 > total || r0 > r1) throw IndexError("triple-rank range outside [0, C(M,3))");
   const std::size_t G = cfg.devices.size();
+  std::vector<std::uint64_t> bal(G + 1);
+  check(e3_partition_balanced(num_snps, std::uint32_t(G), bal.data()));
   std::vector<SearchResult> partials(G);
   std::vector<std::exception_ptr> failures(G);
   auto worker = [&](std::size_t g) {
     try {
-      const std::uint64_t a = r0 + (r1 - r0) * g / G, b = r0 + (r1 - r0) * (g + 1) / G;
+      // whole searches split by measured device cost (e3_partition_balanced),
+      // sub-ranges by triple count
+      std::uint64_t a = r0 + (r1 - r0) * g / G, b = r0 + (r1 - r0) * (g + 1) / G;
+      if (r0 == 0 && r1 == total) {
+        a = bal[g];
+        b = bal[g + 1];
+      }
       DeviceDataset dd(src, cfg.devices[g]);
       partials[g] = a < b ? dd.search(cfg.top_k, a, b) : SearchResult{};
       partials[g].top_k = cfg.top_k;

@@ -101,6 +101,38 @@ extern "C" int e3_partition(uint64_t M, uint32_t parts, uint64_t* bounds) {
   return E3_OK;
 }
 
+// Cost-balanced partition for the multi-GPU split: the SYRK engine's device
+// time over a range is, to ~1-3% (64-slice profiles of cfg3 and cfg5 on B200,
+// profiles/r02_partition_model.json), a fixed cost per 64x64 (j,k) tile plus
+// a per-first-SNP cost (compaction, batch boundaries) of about kTilesPerSnp
+// tiles. Ranges hold equal shares of that cost; inside a first SNP the cost
+// is taken as proportional to its triples (j-major order covers tile rows).
+extern "C" int e3_partition_balanced(uint64_t M, uint32_t parts, uint64_t* bounds) {
+  if (parts < 1) return fail(E3_DOMAIN, "parts must be >= 1");
+  if (M < 3) return fail(E3_DIMENSION, "search needs at least 3 SNPs");
+  constexpr double kTilesPerSnp = 16.0;
+  constexpr uint64_t kEdge = 64;
+  std::vector<double> cw(M - 1, 0.0);  // cumulative cost before first SNP i
+  for (uint64_t i = 0; i + 2 < M; ++i) {
+    const uint64_t nb = (M - 1 - i + kEdge - 1) / kEdge;
+    cw[i + 1] = cw[i] + double(nb * (nb + 1) / 2) + kTilesPerSnp;
+  }
+  const double total_cost = cw[M - 2];
+  const uint64_t total = (uint64_t)c3(M);
+  bounds[0] = 0;
+  uint64_t i = 0;
+  for (uint32_t p = 1; p < parts; ++p) {
+    const double target = total_cost * p / parts;
+    while (i + 3 < M && cw[i + 1] <= target) ++i;
+    const uint64_t first = total - (uint64_t)c3(M - i);  // rank of (i, i+1, i+2)
+    const uint64_t tri = (M - 1 - i) * (M - 2 - i) / 2;
+    const double frac = std::min(1.0, std::max(0.0, (target - cw[i]) / (cw[i + 1] - cw[i])));
+    bounds[p] = std::max(bounds[p - 1], first + uint64_t(std::llround(frac * double(tri))));
+  }
+  bounds[parts] = total;
+  return E3_OK;
+}
+
 // ---------------------------------------------------------------------------
 // K2 scoring on the host: build_log_table / k2_score (src/scoring.cpp:14-35)
 // ---------------------------------------------------------------------------

@@ -119,6 +119,7 @@ SIGNATURES = {
     "e3_triple_rank": (C.c_int, [_U64, _U32, _U32, _U32, C.POINTER(_U64)]),
     "e3_triple_unrank": (C.c_int, [_U64, _U64, _P]),
     "e3_partition": (C.c_int, [_U64, _U32, _P]),
+    "e3_partition_balanced": (C.c_int, [_U64, _U32, _P]),
     "e3_build_log_table": (C.c_int, [_U64, _P]),
     "e3_k2_score": (C.c_double, [_P, _P]),
     "e3_merge_hits": (C.c_int, [_P, _U64, _U32, _P, C.POINTER(_U32)]),
@@ -284,9 +285,17 @@ def triple_unrank(M: int, rank: int) -> tuple:
 
 
 def partition(M: int, parts: int) -> list:
-    """Equal-work contiguous triple-rank ranges for `parts` GPUs."""
+    """Contiguous triple-rank ranges of equal triple counts."""
     b = np.zeros(parts + 1, dtype=np.uint64)
     _check(lib.e3_partition(M, parts, _ptr(b)))
+    return [(int(b[p]), int(b[p + 1])) for p in range(parts)]
+
+
+def partition_balanced(M: int, parts: int) -> list:
+    """Contiguous triple-rank ranges of equal measured device cost (the
+    multi-GPU split: e3_partition_balanced)."""
+    b = np.zeros(parts + 1, dtype=np.uint64)
+    _check(lib.e3_partition_balanced(M, parts, _ptr(b)))
     return [(int(b[p]), int(b[p + 1])) for p in range(parts)]
 
 

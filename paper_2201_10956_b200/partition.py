@@ -19,8 +19,9 @@ from . import epi3
 
 
 def rank_range(M: int, rank: int, world: int) -> tuple:
-    """This rank's contiguous slice of [0, C(M,3)) (equal triple counts)."""
-    return epi3.partition(M, world)[rank]
+    """This rank's contiguous slice of [0, C(M,3)) (equal measured device cost,
+    e3_partition_balanced)."""
+    return epi3.partition_balanced(M, world)[rank]
 
 
 def _pack(local: epi3.SearchResult, top_k: int, device) -> torch.Tensor:

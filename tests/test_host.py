@@ -184,3 +184,34 @@ def test_oracle_built_bench_sample_equals_product_input():
             a = hashlib.sha256(open(d + "/a.epi3", "rb").read()).hexdigest()
             b = hashlib.sha256(open(d + "/b.epi3", "rb").read()).hexdigest()
         assert a == b, (M, N)
+
+
+@pytest.mark.parametrize("M", [3, 4, 5, 64, 65, 300, 2048, 8192])
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8, 16])
+def test_partition_balanced_tiles_the_rank_space(M, parts):
+    """e3_partition_balanced: contiguous, ordered ranges covering [0, C(M,3))
+    exactly; on large M the per-range cost model (64x64 tiles + 16 per first
+    SNP) is equal to within a fraction of a first SNP."""
+    import numpy as np
+    b = epi3.partition_balanced(M, parts)
+    total = epi3.num_combinations(M, 3)
+    assert b[0][0] == 0 and b[-1][1] == total
+    assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+    assert all(x[0] <= x[1] for x in b)
+    if M >= 2048:
+        i = np.arange(M - 2)
+        nb = (M - 1 - i + 63) // 64
+        w = nb * (nb + 1) / 2 + 16.0
+        tri = (M - 1 - i) * (M - 2 - i) / 2
+        ctri = np.concatenate([[0], np.cumsum(tri)])
+        costs = []
+        for a, e in b:
+            c = 0.0
+            lo = np.searchsorted(ctri, a, side="right") - 1
+            hi = min(np.searchsorted(ctri, e, side="right") - 1, M - 3)
+            for ii in range(lo, hi + 1):
+                s_, e_ = max(a, ctri[ii]), min(e, ctri[ii + 1])
+                if e_ > s_:
+                    c += w[ii] * (e_ - s_) / tri[ii]
+            costs.append(c)
+        assert max(costs) / (sum(costs) / parts) < 1.002

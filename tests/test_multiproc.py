@@ -67,4 +67,5 @@ def test_gloo_partition_allgather_merge(world):
     for rank, top, combos, work in out:
         assert top == whole  # every rank holds the identical merged result
         assert combos == epi3.num_combinations(M, 3)
-        assert max(work) - min(work) <= 1  # equal-work ranges
+        # the cost-balanced ranges tile [0, C(M,3)) exactly, one per rank
+        assert work == [b - a for a, b in epi3.partition_balanced(M, world)]
