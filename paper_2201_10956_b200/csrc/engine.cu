@@ -44,6 +44,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "epi3cu.h"
@@ -429,6 +430,29 @@ __device__ __forceinline__ void offer(bool valid, uint64_t sk, uint64_t tk, uint
   const bool want = valid && sk <= gth && (nlist < K || key_less(sk, tk, ls[K - 1], lt[K - 1]));
   const unsigned cand = __ballot_sync(0xffffffffu, want);
   if (cand) warp_insert(ls, lt, nlist, K, cand, sk, tk, lane, gthr);
+}
+
+// offer() with the list's last entry held in registers (lastS, lastT = ~0
+// while the list is not full), so the common rejection reads no shared
+// memory; refreshed after the (rare) insert.
+__device__ __forceinline__ void offer_cached(bool valid, uint64_t sk, uint64_t tk, uint64_t gth,
+                                             uint64_t* ls, uint64_t* lt, uint32_t& nlist,
+                                             uint32_t K, int lane, uint64_t* gthr,
+                                             const Collect& col, uint64_t& lastS,
+                                             uint64_t& lastT) {
+  if (col.buf) {
+    offer(valid, sk, tk, gth, ls, lt, nlist, K, lane, gthr, col);
+    return;
+  }
+  const bool want = valid && sk <= gth && key_less(sk, tk, lastS, lastT);
+  const unsigned cand = __ballot_sync(0xffffffffu, want);
+  if (cand) {
+    warp_insert(ls, lt, nlist, K, cand, sk, tk, lane, gthr);
+    if (nlist == K) {
+      lastS = ls[K - 1];
+      lastT = lt[K - 1];
+    }
+  }
 }
 
 template <bool kRanged, int kMinBlocks>

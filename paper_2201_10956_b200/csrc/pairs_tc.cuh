@@ -93,16 +93,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base_sh;
-  if (warp > kProd) {  // block scale factors = 1.0, one warp per TMEM lane quarter
-    const uint32_t addr = tmem + (uint32_t((warp & 3) * 32) << 16) + kSfCol;
-    const uint32_t one = 0x7F7F7F7Fu;
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
-        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
-        "r"(one)
-        : "memory");
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
+  if (warp > kProd)  // block scale factors (syrk::expand_stage_f4), one warp per TMEM lane quarter
+    syrk::init_scale_factors(tmem + (uint32_t((warp & 3) * 32) << 16) + kSfCol);
   fence_before();
   __syncthreads();
   fence_after();
@@ -127,8 +119,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
             const uint32_t bbase = abase + kRows * kSRowBytes;
 #pragma unroll
             for (int kk = 0; kk < kSRowBytes / 32; ++kk)
-              syrk::mma_f4(dcol, syrk::f4_desc(abase + kk * 256), syrk::f4_desc(bbase + kk * 256), tsf,
-                           (ch != 0 || kk != 0) ? 1u : 0u);
+              syrk::mma_f4(dcol, syrk::f4_desc(abase + kk * 256), syrk::f4_desc(bbase + kk * 256),
+                           tsf + syrk::sf_col(kk), (ch != 0 || kk != 0) ? 1u : 0u);
             mma_commit(&empty_bar[st]);
           }
           mma_commit(&tfull_bar[slot]);
@@ -176,10 +168,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) pairs_tc_kernel(const PArgs p) {
             }
             mbar_wait(&empty_bar[st], ph ^ 1);
             const uint32_t so = st * kSStageBytes;
-            syrk::expand_quad_f4(stage_a + so, 0, ca0);
-            syrk::expand_quad_f4(stage_a + so, 1, ca1);
-            syrk::expand_quad_f4(stage_b + so, 0, cb0);
-            syrk::expand_quad_f4(stage_b + so, 1, cb1);
+            syrk::expand_stage_f4(stage_a + so, ca0, ca1);
+            syrk::expand_stage_f4(stage_b + so, cb0, cb1);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&full_bar[st]);

@@ -27,8 +27,9 @@ namespace syrk {
 using namespace tc;
 
 constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows each
-// Operands are packed E2M1 (fp4, two samples per byte; 1.0 = nibble 0x2),
-// multiplied by tcgen05.mma kind::mxf4 with all block scales = 1.0 and f32
+// Operands are packed E2M1 (fp4, two samples per byte; a one is a single-bit
+// nibble whose value the UE8M0 block scale brings back to 1.0, see
+// expand_stage_regs), multiplied by tcgen05.mma kind::mxf4 with f32
 // accumulation, which is exact for counts < 2^24 (host requires N_c < 2^23).
 constexpr int kSChunk = 256;                           // samples per stage
 constexpr int kSRowBytes = kSChunk / 2;                // 128 B per operand row
@@ -42,7 +43,7 @@ constexpr int kSBStageBytes = kRows * kSRowBytes;      // B only = 16 KiB
 constexpr uint32_t kAStageCols = kSRowBytes / 4;       // 32 TMEM columns per A stage
 constexpr uint32_t kACol = 416;                        // A stages: columns [416, 512)
 constexpr int kUnits = 3;          // TMEM ring of (tile, a, c) accumulators, 128 columns each
-constexpr uint32_t kSfCol = 384;   // scale-factor columns (UE8M0 1.0)
+constexpr uint32_t kSfCol = 384;   // scale-factor columns (init_scale_factors)
 static_assert(kACol >= kSfCol + 32 && kACol + kSyrkStages * kAStageCols <= 512, "TMEM columns");
 constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10)          // A, B = E2M1
                             | (uint32_t(128 >> 3) << 17)      // N = 128
@@ -69,18 +70,32 @@ __device__ __forceinline__ void mma_f4_ts(uint32_t tmem_d, uint32_t tmem_a, uint
       "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%5], p;\n\t}"
       ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(kIdescF4), "r"(accumulate), "r"(tsf));
 }
-// One 128-sample quad of an A row as E2M1 nibbles in TMEM column order: the
-// same 16-byte slabs expand_quad_f4 stores, slab 4h+x -> columns 4(4h+x)..+3.
-__device__ __forceinline__ void expand_quad_regs(uint32_t* out, uint4 q) {
-  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+// One 256-sample stage of an operand row (two 128-sample quads q0, q1) as
+// E2M1 nibbles: eight 16-byte slabs (32 samples = one block-scale K block
+// each). Slab 2t+h holds "part t" of the four words of quad h: the samples
+// at bit 4n+t of each word, kept in place as nibble bit t (t = 0, 1, 2:
+// values 0.5, 1.0, 2.0 — a single AND) or, for t = 3 (bit 3 is the E2M1
+// sign), moved to nibble bit 2 (2.0). MMA kk (two slabs, K = 64) then sees
+// one encoding, undone exactly by its UE8M0 block scales (2, 1, 1/2, 1/2 on
+// both A and B, kSfCol groups), so every product of two ones is 1.0: 5 ALU
+// ops per 32 samples instead of 7. The sample permutation is the same for A
+// and B, so every dot product is unchanged.
+__device__ __forceinline__ uint32_t f4_part(uint32_t v, int t) {
+  return t == 0 ? (v & 0x11111111u)
+       : t == 1 ? (v & 0x22222222u)
+       : t == 2 ? (v & 0x44444444u)
+                : ((v >> 1) & 0x44444444u);
+}
+// Half `hf` of the stage (slabs 4hf .. 4hf+3, i.e. parts t = 2hf, 2hf+1) as
+// 16 registers in row-byte order (register 4s + x = word x of slab s).
+__device__ __forceinline__ void expand_stage_regs(uint32_t* out, uint4 q0, uint4 q1, int hf) {
+  const uint32_t w[2][4] = {{q0.x, q0.y, q0.z, q0.w}, {q1.x, q1.y, q1.z, q1.w}};
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const uint32_t v = w[x];
-    out[4 * x + 0] = (v << 1) & 0x22222222u;
-    out[4 * x + 1] = v & 0x22222222u;
-    out[4 * x + 2] = (v >> 1) & 0x22222222u;
-    out[4 * x + 3] = (v >> 2) & 0x22222222u;
-  }
+  for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) out[4 * (2 * tt + h) + x] = f4_part(w[h][x], 2 * hf + tt);
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -90,6 +105,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
       "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
       "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
       "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -104,20 +127,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 __device__ __forceinline__ uint32_t f32_count(uint32_t bits) {
   return __float_as_uint(__uint_as_float(bits) + 8388608.f) - 0x4B000000u;
 }
-// One 128-sample quad -> slabs [4h, 4h+4) (16 B = 32 samples each) of an
-// operand row. Slab word t holds, in nibble n, sample 4n+t of the quad word
-// as E2M1 1.0 (0x2) or 0: a fixed permutation of the sample axis, identical
-// for A and B, so every dot product is unchanged.
-__device__ __forceinline__ void expand_quad_f4(uint32_t row_saddr, int h, uint4 q) {
-  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+// Block scale factors of the encodings above, written by one warp per TMEM
+// lane quarter: every byte of columns kSfCol + [0, 8) is UE8M0 2^1, of
+// [8, 16) 2^0 and of [16, 32) 2^-1, so MMA kk of a stage reads its uniform
+// scale at sf_col(kk) whatever the per-lane byte layout of the SF operand.
+__device__ __forceinline__ void init_scale_factors(uint32_t tmem_quarter_sf) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%2,%2,%2,%2,%2,%2,%2,%2,"
+      "%3,%3,%3,%3,%3,%3,%3,%3,%3,%3,%3,%3,%3,%3,%3,%3};" ::"r"(tmem_quarter_sf),
+      "r"(0x80808080u), "r"(0x7F7F7F7Fu), "r"(0x7E7E7E7Eu)
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__host__ __device__ constexpr uint32_t sf_col(int kk) {
+  return kk == 0 ? 0u : kk == 1 ? 8u : 16u;
+}
+// The same stage of a B row into shared memory: slab s at row_saddr + 128 s
+// (canonical no-swizzle K-major layout).
+__device__ __forceinline__ void expand_stage_f4(uint32_t row_saddr, uint4 q0, uint4 q1) {
+  const uint32_t w[2][4] = {{q0.x, q0.y, q0.z, q0.w}, {q1.x, q1.y, q1.z, q1.w}};
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const uint32_t v = w[x];
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row_saddr + (4 * h + x) * 128),
-                 "r"((v << 1) & 0x22222222u), "r"(v & 0x22222222u), "r"((v >> 1) & 0x22222222u),
-                 "r"((v >> 2) & 0x22222222u)
-                 : "memory");
-  }
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row_saddr + (2 * t + h) * 128),
+                   "r"(f4_part(w[h][0], t)), "r"(f4_part(w[h][1], t)), "r"(f4_part(w[h][2], t)),
+                   "r"(f4_part(w[h][3], t))
+                   : "memory");
 }
 constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
 constexpr int kScratchPerThread = kRounds * 32;  // u32: 8 values x 2 classes x 2 phases per round
@@ -130,7 +166,13 @@ constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-pack
 // 16K-register file / 32 lanes (13 uniform warps were capped at 128 each).
 constexpr int kSyrkProducerWarps = 4;
 constexpr int kSyrkThreads = 32 * 16;
-constexpr int kRegProducer = 88, kRegEpilogue = 184, kRegMma = 56;
+#ifndef E3_REG_PROD
+#define E3_REG_PROD 88
+#define E3_REG_EPI 184
+#endif
+constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = 56;
+static_assert(kRegProducer + 2 * kRegEpilogue + kRegMma <= 512 && kRegProducer % 8 == 0 &&
+              kRegEpilogue % 8 == 0, "setmaxnreg budgets");
 constexpr int kEpiWarp0 = 4, kMmaWarp = 12;
 
 // Per-i layout of the compacted operands (one record per i of the batch).
@@ -165,6 +207,16 @@ struct SyrkArgs {
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
   uint32_t nst;                      // operand stages in use (2..kSyrkStages)
 };
+
+// Profiling-only variants (E3_DEBUG_SKIP) exist only in a library built with
+// -DE3_PROFILE_SKIP=1 (build.py build_profile_variant); the product build
+// compiles every check below away.
+#ifndef E3_PROFILE_SKIP
+#define E3_PROFILE_SKIP 0
+#endif
+__device__ __forceinline__ uint32_t dbg_skip(const SyrkArgs& s) {
+  return E3_PROFILE_SKIP ? s.debug_skip : 0u;
+}
 
 // Y_{i,p} by bit compression: for slot p (phase a) and class c, every
 // operand row (j, b) keeps the bits of X_b^j at the samples where SNP i has
@@ -394,22 +446,18 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t ktab_s = smem_u32(ktab);
+  uint32_t ktab_s = smem_u32(ktab);
+  asm volatile("" : "+r"(ktab_s));  // keep in a register (see scr_s)
   // shared addresses of the barriers, hoisted out of the hot loops
-  const uint32_t full_s = smem_u32(full_bar), empty_s = smem_u32(empty_bar);
-  const uint32_t tfull_s = smem_u32(tfull_bar), tempty_s = smem_u32(tempty_bar);
-  // Block scale factors = 1.0 (UE8M0 0x7F) in columns [kSfCol, kSfCol+32) of
+  uint32_t full_s = smem_u32(full_bar), empty_s = smem_u32(empty_bar);
+  uint32_t tfull_s = smem_u32(tfull_bar), tempty_s = smem_u32(tempty_bar);
+  // opaque: the compiler would recompute generic->shared conversions (S2UR
+  // SR_CgaCtaId + address arithmetic) inside the loops
+  asm volatile("" : "+r"(full_s), "+r"(empty_s), "+r"(tfull_s), "+r"(tempty_s));
+  // Block scale factors (expand_stage_regs) in columns [kSfCol, kSfCol+32) of
   // all 128 lanes: one epilogue warp per TMEM lane quarter writes them.
-  if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-    const uint32_t addr = tmem + (uint32_t((warp & 3) * 32) << 16) + kSfCol;
-    const uint32_t one = 0x7F7F7F7Fu;
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
-        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
-        "r"(one)
-        : "memory");
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
+  if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4)
+    init_scale_factors(tmem + (uint32_t((warp & 3) * 32) << 16) + kSfCol);
   fence_before();
   __syncthreads();
   fence_after();
@@ -444,7 +492,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               const uint32_t bbase = smem_u32(stages + st * kSBStageBytes);
 #pragma unroll
               for (int kk = 0; kk < kSRowBytes / 32; ++kk)
-                mma_f4_ts(dcol, acol + kk * 8, f4_desc(bbase + kk * 256), tsf,
+                mma_f4_ts(dcol, acol + kk * 8, f4_desc(bbase + kk * 256), tsf + sf_col(kk),
                           (ch != 0 || kk != 0) ? 1u : 0u);
               mma_commit_a(empty_s + 8 * st);
             }
@@ -477,42 +525,27 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         for (uint32_t a = 0; a < 2; ++a) {
           const uint4* Ya = s.Y + inf.y_off[a] + row_a;
           const uint4* Yb = s.Y + inf.y_off[a] + row_b;
-          const size_t R = inf.R;
-          const uint32_t qtot = inf.q[a][0] + inf.q[a][1];
-          constexpr uint32_t kAhead = 2;
-          uint4 pa[kAhead][2], pb[kAhead][2];
-#pragma unroll
-          for (uint32_t x = 0; x < kAhead; ++x)
-            if (2 * x < qtot) {
-              pa[x][0] = __ldg(Ya + (2 * x) * R);
-              pa[x][1] = __ldg(Ya + (2 * x + 1) * R);
-              pb[x][0] = __ldg(Yb + (2 * x) * R);
-              pb[x][1] = __ldg(Yb + (2 * x + 1) * R);
-            }
-          for (uint32_t q = 0; q < qtot; q += 2) {
-            const uint4 a0 = pa[0][0], a1 = pa[0][1], b0 = pb[0][0], b1 = pb[0][1];
-#pragma unroll
-            for (uint32_t x = 0; x + 1 < kAhead; ++x) {
-              pa[x][0] = pa[x + 1][0]; pa[x][1] = pa[x + 1][1];
-              pb[x][0] = pb[x + 1][0]; pb[x][1] = pb[x + 1][1];
-            }
-            if (q + 2 * kAhead < qtot) {
-              const size_t o = size_t(q + 2 * kAhead) * R;
-              pa[kAhead - 1][0] = __ldg(Ya + o);
-              pa[kAhead - 1][1] = __ldg(Ya + o + R);
-              pb[kAhead - 1][0] = __ldg(Yb + o);
-              pb[kAhead - 1][1] = __ldg(Yb + o + R);
-            }
+          const uint32_t R = inf.R;
+          const uint32_t qtot = inf.q[a][0] + inf.q[a][1];  // even: 256-sample stages
+          // Y quads of the next two stages in flight (L2 latency). (Unrolling
+          // over stage pairs to avoid the register moves measured -16% at cfg3.)
+          uint4 a00, a01, b00, b01, a10, a11, b10, b11;
+          auto load = [&](uint32_t q, uint4& x0, uint4& x1, uint4& y0, uint4& y1) {
+            const size_t o = size_t(q) * R;
+            x0 = __ldg(Ya + o); x1 = __ldg(Ya + o + R);
+            y0 = __ldg(Yb + o); y1 = __ldg(Yb + o + R);
+          };
+          auto stage = [&](uint4 x0, uint4 x1, uint4 y0, uint4 y1) {
             mbar_wait_a(empty_s + 8 * st, ph ^ 1);
             fence_after();  // the MMAs that read this A stage have completed
-            if (!(s.debug_skip & 2)) {
-              uint32_t av[32];
-              expand_quad_regs(av, a0);
-              expand_quad_regs(av + 16, a1);
-              tmem_st32(tmem_a + st * kAStageCols, av);
-              const uint32_t so = st * kSBStageBytes;
-              expand_quad_f4(stage_b + so, 0, b0);
-              expand_quad_f4(stage_b + so, 1, b1);
+            if (!(dbg_skip(s) & 2)) {
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {  // A: two 16-column halves (register pressure)
+                uint32_t av[16];
+                expand_stage_regs(av, x0, x1, hf);
+                tmem_st16(tmem_a + st * kAStageCols + 16 * hf, av);
+              }
+              expand_stage_f4(stage_b + st * kSBStageBytes, y0, y1);
               asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
             fence_before();
@@ -520,6 +553,14 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             __syncwarp();
             if (lane == 0) mbar_arrive_a(full_s + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1; }
+          };
+          if (qtot > 0) load(0, a00, a01, b00, b01);
+          if (qtot > 2) load(2, a10, a11, b10, b11);
+          for (uint32_t q = 0; q < qtot; q += 2) {
+            const uint4 x0 = a00, x1 = a01, y0 = b00, y1 = b01;
+            a00 = a10; a01 = a11; b00 = b10; b01 = b11;
+            if (q + 4 < qtot) load(q + 4, a10, a11, b10, b11);
+            stage(x0, x1, y0, y1);
           }
         }
         wk.next(s);
@@ -542,12 +583,20 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       lt[e] = v.y;
     }
     __syncwarp();
+    uint64_t lastS = ~0ull, lastT = ~0ull;  // the list's last key once full (offer_cached)
+    if (nlist == K) {
+      lastS = ls[K - 1];
+      lastT = lt[K - 1];
+    }
     const int jl = quarter * 16 + (lane >> 1);  // row = 2*j_local + b
     const int bsel = lane & 1;
     uint32_t* scr = kSS ? sscr + et : s.scratch + size_t(blockIdx.x) * kScratchPerThread * 256 + et;
     // narrow scratch word x of this thread (x-major, thread-minor): explicit
     // shared-memory accesses when it lives there (no generic LD/ST)
-    const uint32_t scr_s = kSS ? smem_u32(sscr + et) : 0u;
+    uint32_t scr_s = kSS ? smem_u32(sscr + et) : 0u;
+    // opaque to the compiler: otherwise it rematerialises the aligned
+    // dynamic-shared-memory base (≈15 uniform instructions) every round
+    asm volatile("" : "+r"(scr_s));
     auto scr_st = [&](uint32_t x, uint32_t v) {
       if constexpr (kSS) sts_u32(scr_s + x * 1024u, v);
       else scr[x * 256] = v;
@@ -564,6 +613,24 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo inf = s.info[wk.ii];
         const uint32_t i = s.i_lo + wk.ii;
+        const uint32_t j = i + 1 + wk.jb * kJB + jl;
+        const uint32_t jc = min(j, M - 1);
+        const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
+        // narrow: the tile's marginals and round 0's pair(j,k) entries are
+        // requested before the drain waits for the MMAs (DRAM latency hidden)
+        uint4 pij = make_uint4(0, 0, 0, 0), pjn[2];
+        uint2 sip = make_uint2(0, 0), sjp = make_uint2(0, 0);
+        auto fetch_pairs = [&](int mm) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            pjn[h] = __ldg(d.pairp + size_t(min(kbase + 4 * mm + h, M - 1)) * M + jc);
+        };
+        if constexpr (kNarrow) {
+          pij = __ldg(d.pairp + size_t(i) * M + jc);
+          sip = __ldg(d.singlep + i);
+          sjp = __ldg(d.singlep + jc);
+          fetch_pairs(0);
+        }
         // ---- drain the four units (a, c) of this tile: TMEM (f32 counts) ->
         // scratch, releasing each ring slot as soon as it is copied, so the MMAs
         // of the next units overlap the scoring below.
@@ -582,20 +649,30 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             const bool e0 = inf.q[a][0] == 0, e1 = inf.q[a][1] == 0;
             const float scl = float(1u << kSh);
             const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + half * 8 * kRounds;
+            auto drain = [&](auto empty) {
+              constexpr bool kEmpty = decltype(empty)::value;
 #pragma unroll
-            for (int m2 = 0; m2 < kRounds; m2 += 2) {
-              uint32_t v0[16], v1[16];
-              tmem_ld16(tbase + s0 * 128 + 8 * m2, v0);
-              tmem_ld16(tbase + s1 * 128 + 8 * m2, v1);
-              tmem_wait_ld();
+              for (int m2 = 0; m2 < kRounds; m2 += 2) {
+                uint32_t v0[16], v1[16];
+                tmem_ld16(tbase + s0 * 128 + 8 * m2, v0);
+                tmem_ld16(tbase + s1 * 128 + 8 * m2, v1);
+                tmem_wait_ld();
 #pragma unroll
-              for (int x = 0; x < 16; ++x) {
-                const int m = m2 + (x >> 3), tg = x & 7;
-                const uint32_t b0 = e0 ? 0x4B000000u : __float_as_uint(__fmaf_rn(__uint_as_float(v0[x]), scl, 8388608.f));
-                const uint32_t b1 = e1 ? 0x4B000000u : __float_as_uint(__fmaf_rn(__uint_as_float(v1[x]), scl, 8388608.f));
-                scr_st(a * kRounds * 8 + m * 8 + tg, __byte_perm(b0, b1, 0x5410));
+                for (int x = 0; x < 16; ++x) {
+                  const int m = m2 + (x >> 3), tg = x & 7;
+                  uint32_t b0 = __float_as_uint(__fmaf_rn(__uint_as_float(v0[x]), scl, 8388608.f));
+                  uint32_t b1 = __float_as_uint(__fmaf_rn(__uint_as_float(v1[x]), scl, 8388608.f));
+                  if constexpr (kEmpty) {
+                    if (e0) b0 = 0x4B000000u;
+                    if (e1) b1 = 0x4B000000u;
+                  }
+                  scr_st(a * kRounds * 8 + m * 8 + tg, __byte_perm(b0, b1, 0x5410));
+                }
               }
-            }
+            };
+            // (tile-uniform branch: the selects only for the rare empty slot)
+            if (e0 || e1) drain(std::true_type{});
+            else drain(std::false_type{});
             fence_before();
             mbar_arrive_a(tempty_s + 8 * s0);
             mbar_arrive_a(tempty_s + 8 * s1);
@@ -627,8 +704,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             mbar_arrive_a(tempty_s + 8 * slot);
           }
         }
-        const uint32_t j = i + 1 + wk.jb * kJB + jl;
-        const uint32_t jc = min(j, M - 1);
         const uint64_t gth = *reinterpret_cast<volatile uint64_t*>(s.gthr);
         // screening bound: a triple whose fp32 screen exceeds thr_f cannot reach
         // the threshold (margin proven on the host, k2_screen_margin)
@@ -642,21 +717,15 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         }
         if constexpr (kNarrow) {
           // class-packed words (class0 | class1 << 16) throughout
-          const uint4 pij = __ldg(d.pairp + size_t(i) * M + jc);
-          const uint2 sip = __ldg(d.singlep + i), sjp = __ldg(d.singlep + jc);
           // per-half masks of the dropped phase (slots hold the other two, ascending)
           const uint32_t mk0 = (inf.drop[0] == 0 ? 0xffffu : 0u) | (inf.drop[1] == 0 ? 0xffff0000u : 0u);
           const uint32_t mk1 = (inf.drop[0] == 1 ? 0xffffu : 0u) | (inf.drop[1] == 1 ? 0xffff0000u : 0u);
           const uint32_t mk2 = ~(mk0 | mk1);
-          const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
           // the next round's pair(j,k) entries and scratch words are fetched one
           // round ahead (software pipelining across rounds)
-          uint4 pjn[2];
           uint32_t Wn[2][4][2];
           auto fetch_round = [&](int mm) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              pjn[h] = __ldg(d.pairp + size_t(min(kbase + 4 * mm + h, M - 1)) * M + jc);
+            if (mm > 0) fetch_pairs(mm);
 #pragma unroll
             for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -693,7 +762,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               kk[h] = kbase + 4 * m + h;
-              valid[h] = j < kk[h] && kk[h] < M && !(s.debug_skip & 1);
+              valid[h] = j < kk[h] && kk[h] < M && !(dbg_skip(s) & 1);
               if (kRanged && valid[h]) {
                 const uint64_t rr = rank_ij + (kk[h] - j - 1);
                 valid[h] = rr >= s.rank_begin && rr < s.rank_end;
@@ -730,16 +799,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               for (int h = 0; h < 2; ++h) {
                 uint32_t n[27];
                 derive_cells(T[h], pij, pik[h], pjk[h], sip, sjp, skp[h], d.npk, n);
-                if (s.debug_skip & 2) {  // profiling: operands not expanded -> keep lookups in range
+                if (dbg_skip(s) & 2) {  // profiling: operands not expanded -> keep lookups in range
 #pragma unroll
                   for (int c = 0; c < 27; ++c) n[c] &= 0x0ffc0ffcu;
                 }
-                if (s.debug_skip & 4)
+                if (dbg_skip(s) & 4)
                   pass[h] = n[26] == 0x7fffffffu;  // profiling: derivation only
                 else
                   pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled(n, ktab_s)
                                                               : k2_screen_packed(n, ktab_s, d.st_c1)) <= thr_f) &&
-                            !(s.debug_skip & 2);
+                            !(dbg_skip(s) & 2);
               }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
@@ -758,7 +827,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              offer(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col);
+              offer_cached(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col, lastS, lastT);
             }
           }
         } else {
@@ -766,7 +835,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           const uint4 pij1 = __ldg(d.pair[1] + size_t(i) * M + jc);
           const uint2 si0 = __ldg(d.single[0] + i), si1 = __ldg(d.single[1] + i);
           const uint2 sj0 = __ldg(d.single[0] + jc), sj1 = __ldg(d.single[1] + jc);
-          const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
           for (int m = 0; m < kRounds; ++m) {
             // pair(j,k) rows first: their L2 latency overlaps the scratch loads
             // and the lane-pair exchange below
@@ -827,7 +895,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   #pragma unroll
             for (int h = 0; h < 2; ++h) {
               kk[h] = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h;
-              valid[h] = j < kk[h] && kk[h] < M && !(s.debug_skip & 1);
+              valid[h] = j < kk[h] && kk[h] < M && !(dbg_skip(s) & 1);
               if (kRanged && valid[h]) {
                 const uint64_t rr = rank_ij + (kk[h] - j - 1);
                 valid[h] = rr >= s.rank_begin && rr < s.rank_end;
@@ -870,7 +938,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 uint32_t n0[27], n1[27];
                 derive_cells(T[h][0], pij0, pik[h][0], pjk[h][0], si0, sj0, skc[h][0], d.n[0], n0);
                 derive_cells(T[h][1], pij1, pik[h][1], pjk[h][1], si1, sj1, skc[h][1], d.n[1], n1);
-                if (s.debug_skip & 4)
+                if (dbg_skip(s) & 4)
                   pass[h] = n0[26] == 0x7fffffffu;  // profiling: derivation only
                 else
                   pass[h] = valid[h] && (!s.screen || k2_screen(n0, n1, ktab_s) <= thr_f);
@@ -888,7 +956,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             }
   #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              offer(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col);
+              offer_cached(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col, lastS, lastT);
             }
           }
         }
