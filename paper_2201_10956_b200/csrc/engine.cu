@@ -213,7 +213,54 @@ __device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_
 // arithmetic is free, and stirling_term's extra FP/MUFU issue cost more than
 // the bank conflicts it saves (measured: cfg3 -6.5%, cfg2 -11%), whereas the
 // unscaled k2_screen_packed gains (cfg5 +1.6%).
+// Two cells per packed f32x2 instruction (FADD2): 1.5 adds per cell instead of 3.
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float f2_hsum(uint64_t a) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  return __fadd_rn(lo, hi);
+}
 __device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_s) {
+#ifndef E3_SCREEN_F32X2
+#define E3_SCREEN_F32X2 1
+#endif
+  if (E3_SCREEN_F32X2) {
+    uint64_t acc[2] = {0ull, 0ull};  // +0.0f x2
+    float last = 0.f;
+#pragma unroll
+    for (int c = 0; c < 26; c += 2) {
+      float g[2][3];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t a0 = G_s + (n[c + e] & 0xffffu), o1 = n[c + e] >> 16;
+        g[e][0] = lds_f32(a0 + o1 + 4);
+        g[e][1] = lds_f32(a0);
+        g[e][2] = lds_f32(G_s + o1);
+      }
+      const uint64_t t = f2_sub(f2_sub(f2_pack(g[0][0], g[1][0]), f2_pack(g[0][1], g[1][1])),
+                                f2_pack(g[0][2], g[1][2]));
+      acc[(c >> 1) & 1] = f2_add(acc[(c >> 1) & 1], t);
+    }
+    {
+      const uint32_t a0 = G_s + (n[26] & 0xffffu), o1 = n[26] >> 16;
+      last = __fsub_rn(__fsub_rn(lds_f32(a0 + o1 + 4), lds_f32(a0)), lds_f32(G_s + o1));
+    }
+    return __fadd_rn(f2_hsum(f2_add(acc[0], acc[1])), last);
+  }
   float s[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int c = 0; c < 27; ++c) {
