@@ -194,26 +194,9 @@ __device__ __forceinline__ float stirling_term(uint32_t mbits, float c1) {
   return __fmaf_rn(ap, lg, cp);
 }
 
-// k2_screen on class-packed cells (narrow path): word = class0 | class1 << 16.
-__device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_s, float c1) {
-  float s[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-  for (int c = 0; c < 27; ++c) {
-    const uint32_t r0 = n[c] & 0xffffu, r1 = n[c] >> 16;
-    const float t = __fsub_rn(__fsub_rn(stirling_term(r0 + r1 + 0x4B000001u, c1), lds_f32(G_s + 4 * r0)),
-                              lds_f32(G_s + 4 * r1));
-    s[c % 3] = __fadd_rn(s[c % 3], t);
-  }
-  return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
-}
-
-// k2_screen_packed for counts scaled by 4 (word = 4 r0 | 4 r1 << 16): the
-// halves are the table byte offsets of G[r0], G[r1], and their sum + 4 that
-// of G[r0 + r1 + 1]. All three terms stay table lookups here: the address
-// arithmetic is free, and stirling_term's extra FP/MUFU issue cost more than
-// the bank conflicts it saves (measured: cfg3 -6.5%, cfg2 -11%), whereas the
-// unscaled k2_screen_packed gains (cfg5 +1.6%).
-// Two cells per packed f32x2 instruction (FADD2): 1.5 adds per cell instead of 3.
+// Packed f32x2 arithmetic (sm_100 FADD2/FFMA2): the screens below handle two
+// cells per instruction. Each lane is an ordinary IEEE rn operation, so the
+// results (and the host's error bound, k2_screen_margin) are unchanged.
 __device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -234,41 +217,107 @@ __device__ __forceinline__ float f2_hsum(uint64_t a) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
   return __fadd_rn(lo, hi);
 }
-__device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_s) {
-#ifndef E3_SCREEN_F32X2
-#define E3_SCREEN_F32X2 1
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float f2_lo(uint64_t a) { return __uint_as_float(uint32_t(a)); }
+__device__ __forceinline__ float f2_hi(uint64_t a) { return __uint_as_float(uint32_t(a >> 32)); }
+__device__ __forceinline__ uint64_t f2_splat(float x) { return f2_pack(x, x); }
+
+// k2_screen on class-packed cells (narrow path): word = class0 | class1 << 16.
+// Two cells per step in f32x2 (the MUFU lg2 stays scalar).
+__device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_s, float c1) {
+  uint64_t acc[2] = {0ull, 0ull};
+  const uint64_t k23 = f2_splat(8388608.f), kl = f2_splat(kLn2), khl = f2_splat(0.5f * kLn2),
+                 kc1 = f2_splat(c1), kh = f2_splat(kHalfLn2Pi);
+#pragma unroll
+  for (int c = 0; c < 26; c += 2) {
+    uint32_t r0[2], r1[2];
+    float g0[2], g1[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      r0[e] = n[c + e] & 0xffffu;
+      r1[e] = n[c + e] >> 16;
+      g0[e] = lds_f32(G_s + 4 * r0[e]);
+      g1[e] = lds_f32(G_s + 4 * r1[e]);
+    }
+    // stirling_term for both cells: m = (2^23 + m) - 2^23, exact
+    const uint64_t mb = (uint64_t(r0[1] + r1[1] + 0x4B000001u) << 32) | (r0[0] + r1[0] + 0x4B000001u);
+    const uint64_t m = f2_sub(mb, k23);
+    float lg0, lg1;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg0) : "f"(f2_lo(m)));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg1) : "f"(f2_hi(m)));
+    const uint64_t ap = f2_fma(m, kl, khl), cp = f2_fma(m, kc1, kh);
+    const uint64_t st = f2_fma(ap, f2_pack(lg0, lg1), cp);
+    const uint64_t t = f2_sub(f2_sub(st, f2_pack(g0[0], g0[1])), f2_pack(g1[0], g1[1]));
+    acc[(c >> 1) & 1] = f2_add(acc[(c >> 1) & 1], t);
+  }
+  const uint32_t r0 = n[26] & 0xffffu, r1 = n[26] >> 16;
+  const float last = __fsub_rn(__fsub_rn(stirling_term(r0 + r1 + 0x4B000001u, c1), lds_f32(G_s + 4 * r0)),
+                               lds_f32(G_s + 4 * r1));
+  return __fadd_rn(f2_hsum(f2_add(acc[0], acc[1])), last);
+}
+
+// k2_screen_packed for counts scaled by 4 (word = 4 r0 | 4 r1 << 16): the
+// halves are the table byte offsets of G[r0], G[r1], and their sum + 4 that
+// of G[r0 + r1 + 1]. All three terms stay table lookups here: the address
+// arithmetic is free, and stirling_term's extra FP/MUFU issue cost more than
+// the bank conflicts it saves (measured: cfg3 -6.5%, cfg2 -11%), whereas the
+// unscaled k2_screen_packed gains (cfg5 +1.6%).
+#ifndef E3_SCALED_STIRLING
+#define E3_SCALED_STIRLING 0
 #endif
-  if (E3_SCREEN_F32X2) {
-    uint64_t acc[2] = {0ull, 0ull};  // +0.0f x2
-    float last = 0.f;
+__device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_s, float c1) {
+  if (E3_SCALED_STIRLING) {
+    uint64_t acc[2] = {0ull, 0ull};
+    const uint64_t kq = f2_splat(0.25f), kb = f2_splat(1.0f - 2097152.0f), kl = f2_splat(kLn2),
+                   khl = f2_splat(0.5f * kLn2), kc1 = f2_splat(c1), kh = f2_splat(kHalfLn2Pi);
 #pragma unroll
     for (int c = 0; c < 26; c += 2) {
-      float g[2][3];
+      uint32_t sb[2];
+      float g0[2], g1[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const uint32_t a0 = G_s + (n[c + e] & 0xffffu), o1 = n[c + e] >> 16;
-        g[e][0] = lds_f32(a0 + o1 + 4);
-        g[e][1] = lds_f32(a0);
-        g[e][2] = lds_f32(G_s + o1);
+        const uint32_t lo = n[c + e] & 0xffffu, hi = n[c + e] >> 16;
+        sb[e] = lo + hi + 0x4B000000u;  // bits of 2^23 + 4 (r0 + r1)
+        g0[e] = lds_f32(G_s + lo);
+        g1[e] = lds_f32(G_s + hi);
       }
-      const uint64_t t = f2_sub(f2_sub(f2_pack(g[0][0], g[1][0]), f2_pack(g[0][1], g[1][1])),
-                                f2_pack(g[0][2], g[1][2]));
+      // m = r0 + r1 + 1 = (2^23 + 4(r0+r1)) / 4 - 2^21 + 1, exact in one FFMA
+      const uint64_t m = f2_fma((uint64_t(sb[1]) << 32) | sb[0], kq, kb);
+      float lg0, lg1;
+      asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg0) : "f"(f2_lo(m)));
+      asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg1) : "f"(f2_hi(m)));
+      const uint64_t ap = f2_fma(m, kl, khl), cp = f2_fma(m, kc1, kh);
+      const uint64_t st = f2_fma(ap, f2_pack(lg0, lg1), cp);
+      const uint64_t t = f2_sub(f2_sub(st, f2_pack(g0[0], g0[1])), f2_pack(g1[0], g1[1]));
       acc[(c >> 1) & 1] = f2_add(acc[(c >> 1) & 1], t);
     }
-    {
-      const uint32_t a0 = G_s + (n[26] & 0xffffu), o1 = n[26] >> 16;
-      last = __fsub_rn(__fsub_rn(lds_f32(a0 + o1 + 4), lds_f32(a0)), lds_f32(G_s + o1));
-    }
+    const uint32_t lo = n[26] & 0xffffu, hi = n[26] >> 16;
+    const float last = __fsub_rn(__fsub_rn(stirling_term(((lo + hi) >> 2) + 0x4B000001u, c1), lds_f32(G_s + lo)),
+                                 lds_f32(G_s + hi));
     return __fadd_rn(f2_hsum(f2_add(acc[0], acc[1])), last);
   }
-  float s[3] = {0.f, 0.f, 0.f};
+  uint64_t acc[2] = {0ull, 0ull};  // +0.0f x2
 #pragma unroll
-  for (int c = 0; c < 27; ++c) {
-    const uint32_t a0 = G_s + (n[c] & 0xffffu), o1 = n[c] >> 16;
-    const float t = __fsub_rn(__fsub_rn(lds_f32(a0 + o1 + 4), lds_f32(a0)), lds_f32(G_s + o1));
-    s[c % 3] = __fadd_rn(s[c % 3], t);
+  for (int c = 0; c < 26; c += 2) {
+    float g[2][3];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const uint32_t a0 = G_s + (n[c + e] & 0xffffu), o1 = n[c + e] >> 16;
+      g[e][0] = lds_f32(a0 + o1 + 4);
+      g[e][1] = lds_f32(a0);
+      g[e][2] = lds_f32(G_s + o1);
+    }
+    const uint64_t t = f2_sub(f2_sub(f2_pack(g[0][0], g[1][0]), f2_pack(g[0][1], g[1][1])),
+                              f2_pack(g[0][2], g[1][2]));
+    acc[(c >> 1) & 1] = f2_add(acc[(c >> 1) & 1], t);
   }
-  return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
+  const uint32_t a0 = G_s + (n[26] & 0xffffu), o1 = n[26] >> 16;
+  const float last = __fsub_rn(__fsub_rn(lds_f32(a0 + o1 + 4), lds_f32(a0)), lds_f32(G_s + o1));
+  return __fadd_rn(f2_hsum(f2_add(acc[0], acc[1])), last);
 }
 
 // fp32 screen of k2_score: sum_c (G[r0+r1+1] - G[r0]) - G[r1] over a
@@ -278,17 +327,26 @@ __device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_
 // screen passes the current threshold are scored exactly with k2_device.
 // G_s: shared-memory (32-bit) address of the table.
 __device__ __forceinline__ float k2_screen(const uint32_t* n0, const uint32_t* n1, uint32_t G_s) {
-  // three independent partial sums (shorter dependency chain); the margin
-  // bound holds for any summation order
-  float s[3] = {0.f, 0.f, 0.f};
+  // two cells per f32x2 step; the margin bound holds for any summation order
+  uint64_t acc[2] = {0ull, 0ull};
 #pragma unroll
-  for (int c = 0; c < 27; ++c) {
-    const uint32_t r0 = n0[c], r1 = n1[c];
-    const float t = __fsub_rn(__fsub_rn(lds_f32(G_s + 4 * (r0 + r1 + 1)), lds_f32(G_s + 4 * r0)),
-                              lds_f32(G_s + 4 * r1));
-    s[c % 3] = __fadd_rn(s[c % 3], t);
+  for (int c = 0; c < 26; c += 2) {
+    float g[2][3];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const uint32_t r0 = n0[c + e], r1 = n1[c + e];
+      g[e][0] = lds_f32(G_s + 4 * (r0 + r1 + 1));
+      g[e][1] = lds_f32(G_s + 4 * r0);
+      g[e][2] = lds_f32(G_s + 4 * r1);
+    }
+    const uint64_t t = f2_sub(f2_sub(f2_pack(g[0][0], g[1][0]), f2_pack(g[0][1], g[1][1])),
+                              f2_pack(g[0][2], g[1][2]));
+    acc[(c >> 1) & 1] = f2_add(acc[(c >> 1) & 1], t);
   }
-  return __fadd_rn(__fadd_rn(s[0], s[1]), s[2]);
+  const uint32_t r0 = n0[26], r1 = n1[26];
+  const float last = __fsub_rn(__fsub_rn(lds_f32(G_s + 4 * (r0 + r1 + 1)), lds_f32(G_s + 4 * r0)),
+                               lds_f32(G_s + 4 * r1));
+  return __fadd_rn(f2_hsum(f2_add(acc[0], acc[1])), last);
 }
 
 // One 32-sample word of one class for one (i, j, k): 8 AND3 + 8 POPC.

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             // then one PRMT joins the low halves of both classes; a class with
             // no samples in this slot has an unwritten accumulator -> constant 0
             const bool e0 = inf.q[a][0] == 0, e1 = inf.q[a][1] == 0;
-            const float scl = float(1u << kSh);
+            const uint64_t scl2 = f2_splat(float(1u << kSh)), k23 = f2_splat(8388608.f);
             const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + half * 8 * kRounds;
             auto drain = [&](auto empty) {
               constexpr bool kEmpty = decltype(empty)::value;
@@ -657,11 +657,20 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 tmem_ld16(tbase + s0 * 128 + 8 * m2, v0);
                 tmem_ld16(tbase + s1 * 128 + 8 * m2, v1);
                 tmem_wait_ld();
+                uint32_t w0[16], w1[16];  // 2^23 + c * 2^kSh, two counts per FFMA2
+#pragma unroll
+                for (int x = 0; x < 16; x += 2) {
+                  const uint64_t p0 = f2_fma(f2_pack(__uint_as_float(v0[x]), __uint_as_float(v0[x + 1])),
+                                             scl2, k23);
+                  const uint64_t p1 = f2_fma(f2_pack(__uint_as_float(v1[x]), __uint_as_float(v1[x + 1])),
+                                             scl2, k23);
+                  w0[x] = uint32_t(p0); w0[x + 1] = uint32_t(p0 >> 32);
+                  w1[x] = uint32_t(p1); w1[x + 1] = uint32_t(p1 >> 32);
+                }
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
                   const int m = m2 + (x >> 3), tg = x & 7;
-                  uint32_t b0 = __float_as_uint(__fmaf_rn(__uint_as_float(v0[x]), scl, 8388608.f));
-                  uint32_t b1 = __float_as_uint(__fmaf_rn(__uint_as_float(v1[x]), scl, 8388608.f));
+                  uint32_t b0 = w0[x], b1 = w1[x];
                   if constexpr (kEmpty) {
                     if (e0) b0 = 0x4B000000u;
                     if (e1) b1 = 0x4B000000u;
@@ -806,7 +815,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 if (dbg_skip(s) & 4)
                   pass[h] = n[26] == 0x7fffffffu;  // profiling: derivation only
                 else
-                  pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled(n, ktab_s)
+                  pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled(n, ktab_s, d.st_c1)
                                                               : k2_screen_packed(n, ktab_s, d.st_c1)) <= thr_f) &&
                             !(dbg_skip(s) & 2);
               }
