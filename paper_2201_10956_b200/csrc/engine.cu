@@ -262,15 +262,16 @@ __device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_
 
 // k2_screen_packed for counts scaled by 4 (word = 4 r0 | 4 r1 << 16): the
 // halves are the table byte offsets of G[r0], G[r1], and their sum + 4 that
-// of G[r0 + r1 + 1]. All three terms stay table lookups here: the address
-// arithmetic is free, and stirling_term's extra FP/MUFU issue cost more than
-// the bank conflicts it saves (measured: cfg3 -6.5%, cfg2 -11%), whereas the
-// unscaled k2_screen_packed gains (cfg5 +1.6%).
-#ifndef E3_SCALED_STIRLING
-#define E3_SCALED_STIRLING 0
+// of G[r0 + r1 + 1], so the table form needs no index arithmetic.
+#ifndef E3_SCREEN_ADDR3
+#define E3_SCREEN_ADDR3 0
 #endif
+// kStir: the pooled term by stirling_term instead of the table, so the table
+// needs only G[0 .. max(N0, N1)] (half the shared memory) and a third of the
+// gathers disappear (cfg3 +2%, cfg2 -5%: the host picks it for large classes).
+template <bool kStir>
 __device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_s, float c1) {
-  if (E3_SCALED_STIRLING) {
+  if constexpr (kStir) {
     uint64_t acc[2] = {0ull, 0ull};
     const uint64_t kq = f2_splat(0.25f), kb = f2_splat(1.0f - 2097152.0f), kl = f2_splat(kLn2),
                    khl = f2_splat(0.5f * kLn2), kc1 = f2_splat(c1), kh = f2_splat(kHalfLn2Pi);
@@ -306,10 +307,19 @@ __device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_
     float g[2][3];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
+#if E3_SCREEN_ADDR3
+      // three ALU ops per cell (lo, hi, lo + hi); the table base (uniform)
+      // folds into each load's [R + UR + imm] address
+      const uint32_t lo = n[c + e] & 0xffffu, hi = n[c + e] >> 16, sm = lo + hi;
+      g[e][0] = lds_f32(G_s + sm + 4);
+      g[e][1] = lds_f32(G_s + lo);
+      g[e][2] = lds_f32(G_s + hi);
+#else
       const uint32_t a0 = G_s + (n[c + e] & 0xffffu), o1 = n[c + e] >> 16;
       g[e][0] = lds_f32(a0 + o1 + 4);
       g[e][1] = lds_f32(a0);
       g[e][2] = lds_f32(G_s + o1);
+#endif
     }
     const uint64_t t = f2_sub(f2_sub(f2_pack(g[0][0], g[1][0]), f2_pack(g[0][1], g[1][1])),
                               f2_pack(g[0][2], g[1][2]));
@@ -1306,46 +1316,31 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
   ds->no_drop = std::getenv("E3_SYRK_NO_DROP") != nullptr;
   if (const char* yb = std::getenv("E3_SYRK_YBUDGET_KIB"))
     ds->y_budget = std::max<size_t>(1, size_t(std::atoll(yb)) * 1024 / sizeof(uint4));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 0>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 0>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 1>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 1>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 2>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 2048)));
-  CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(ds->smem_optin - 2048)));
   {
-    // the shared-scratch kernels run close to the per-block limit: their
-    // dynamic ceiling is the opt-in limit minus their static shared memory
-    cudaFuncAttributes fa{};
+    // every SYRK instantiation may use the opt-in dynamic shared memory; the
+    // shared-scratch kernels run close to the per-block limit, so their
+    // ceiling is the opt-in limit minus their static shared memory
+    const void* global_scr[] = {
+        (const void*)syrk::search_syrk_kernel<false, 0>, (const void*)syrk::search_syrk_kernel<true, 0>,
+        (const void*)syrk::search_syrk_kernel<false, 1>, (const void*)syrk::search_syrk_kernel<true, 1>,
+        (const void*)syrk::search_syrk_kernel<false, 2>, (const void*)syrk::search_syrk_kernel<true, 2>,
+        (const void*)syrk::search_syrk_kernel<false, 3>, (const void*)syrk::search_syrk_kernel<true, 3>};
+    const void* shared_scr[] = {
+        (const void*)syrk::search_syrk_kernel<false, 1, true>, (const void*)syrk::search_syrk_kernel<true, 1, true>,
+        (const void*)syrk::search_syrk_kernel<false, 2, true>, (const void*)syrk::search_syrk_kernel<true, 2, true>,
+        (const void*)syrk::search_syrk_kernel<false, 3, true>, (const void*)syrk::search_syrk_kernel<true, 3, true>};
+    for (const void* f : global_scr)
+      CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(ds->smem_optin - 2048)));
     size_t st_max = 0;
-    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<false, 1, true>));
-    st_max = std::max(st_max, fa.sharedSizeBytes);
-    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<true, 1, true>));
-    st_max = std::max(st_max, fa.sharedSizeBytes);
-    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<false, 2, true>));
-    st_max = std::max(st_max, fa.sharedSizeBytes);
-    CUDA_TRY(cudaFuncGetAttributes(&fa, syrk::search_syrk_kernel<true, 2, true>));
-    st_max = std::max(st_max, fa.sharedSizeBytes);
+    for (const void* f : shared_scr) {
+      cudaFuncAttributes fa{};
+      CUDA_TRY(cudaFuncGetAttributes(&fa, f));
+      st_max = std::max(st_max, fa.sharedSizeBytes);
+    }
     ds->smem_ss_cap = ds->smem_optin - st_max;
-    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 1, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
-    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 1, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
-    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<false, 2, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
-    CUDA_TRY(cudaFuncSetAttribute(syrk::search_syrk_kernel<true, 2, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
+    for (const void* f : shared_scr)
+      CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ds->smem_ss_cap)));
   }
   CUDA_TRY(dmalloc(ds, &ds->gthr, sizeof(uint64_t)));
   CUDA_TRY(dmalloc(ds, &ds->evals, sizeof(unsigned long long)));
@@ -1586,7 +1581,14 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   // table. The screen pays for itself many times over, so when the table does
   // not fit beside four stages the kernel runs with fewer (>= 2).
   const size_t lists_b = size_t(tc::kEpilogueWarps) * 2 * K * sizeof(uint64_t);
-  const size_t tab_b = sizeof(float) * ds->ktab_n;
+  // scaled narrow path with large classes: the screen's pooled term from
+  // Stirling's bound, the table only up to max(N0, N1) (E3_SCREEN_STIRLING=0/1
+  // overrides; measured cfg3 +2%, cfg2 -5%)
+  bool stir = ds->narrow && ds->shift && std::max(ds->N[0], ds->N[1]) >= 4096;
+  if (const char* e = std::getenv("E3_SCREEN_STIRLING")) stir = ds->narrow && ds->shift && std::atoi(e) != 0;
+  const uint32_t ktab_use =
+      stir ? uint32_t((std::max(ds->N[0], ds->N[1]) + 1 + 3) / 4 * 4) : ds->ktab_n;
+  const size_t tab_b = sizeof(float) * ktab_use;
   const size_t cap = ds->smem_optin - 2048;
   uint32_t nst = syrk::kSyrkStages;
   bool screen = !std::getenv("E3_NO_SCREEN");
@@ -1638,6 +1640,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.debug_skip = ds->debug_skip;
     sa.screen = screen ? 1u : 0u;
     sa.nst = nst;
+    sa.ktab_n = ktab_use;
     // batch b's compaction overlaps batch b-1's search; it may reuse buffer
     // b & 1 only once batch b-2's search is done with it
     if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_sdone[buf], 0));
@@ -1656,7 +1659,13 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     // checks; the others run the unranged kernel
     const uint64_t b_lo = first_rank(bt.first), b_hi = first_rank(bt.first + bt.n);
     const bool part = ranged && (r0 > b_lo || r1 < b_hi);
-    if (sscr && ds->shift) {
+    if (sscr && stir) {
+      if (part) syrk::search_syrk_kernel<true, 3, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, 3, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    } else if (stir) {
+      if (part) syrk::search_syrk_kernel<true, 3><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+      else syrk::search_syrk_kernel<false, 3><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
+    } else if (sscr && ds->shift) {
       if (part) syrk::search_syrk_kernel<true, 2, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
       else syrk::search_syrk_kernel<false, 2, true><<<grid, syrk::kSyrkThreads, tsm, st>>>(d, sa);
     } else if (sscr) {

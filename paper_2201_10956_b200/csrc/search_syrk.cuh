@@ -170,6 +170,9 @@ constexpr int kSyrkThreads = 32 * 16;
 #define E3_REG_PROD 88
 #define E3_REG_EPI 184
 #endif
+#ifndef E3_PF
+#define E3_PF 2  // producer: Y quads of this many stages in flight
+#endif
 constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = 56;
 static_assert(kRegProducer + 2 * kRegEpilogue + kRegMma <= 512 && kRegProducer % 8 == 0 &&
               kRegEpilogue % 8 == 0, "setmaxnreg budgets");
@@ -203,9 +206,12 @@ struct SyrkArgs {
   unsigned long long* evals;         // triples evaluated (device counter, add_evals)
   Collect col;                       // large top_k, second pass (offer)
   uint32_t debug_skip;               // profiling only (E3_DEBUG_SKIP): 1 = no scoring, 2 = no
-                                     // operand expansion, 4 = derivation without the screen
+                                     // operand expansion, 4 = derivation without the screen,
+                                     // 8 = no MMAs (barrier protocol only), 16 = conflict-
+                                     // free screen lookups (scaled path)
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
   uint32_t nst;                      // operand stages in use (2..kSyrkStages)
+  uint32_t ktab_n;                   // screening-table entries staged in shared memory
 };
 
 // Profiling-only variants (E3_DEBUG_SKIP) exist only in a library built with
@@ -214,6 +220,15 @@ struct SyrkArgs {
 #ifndef E3_PROFILE_SKIP
 #define E3_PROFILE_SKIP 0
 #endif
+// E3_TIMELINE=1 (profiling builds only): per-role cycle counters printed by
+// the first CTAs at kernel end (waits on each barrier, drain, rounds)
+#ifndef E3_TIMELINE
+#define E3_TIMELINE 0
+#endif
+__device__ __forceinline__ long long tl_clock() {
+  if constexpr (E3_TIMELINE) return clock64();
+  else return 0;
+}
 __device__ __forceinline__ uint32_t dbg_skip(const SyrkArgs& s) {
   return E3_PROFILE_SKIP ? s.debug_skip : 0u;
 }
@@ -393,14 +408,16 @@ struct SWalker {
 // 32-bit arithmetic never carries or borrows across the halves).
 // kMode: 0 = wide, 1 = narrow, 2 = narrow with counts scaled by 4 (every
 // class < 2^14 samples): a packed word then holds the byte offsets of its two
-// counts in the screening table, which saves the index arithmetic per lookup.
+// counts in the screening table, which saves the index arithmetic per lookup;
+// 3 = as 2 with the screen's pooled term from Stirling's bound (the table in
+// shared memory then ends at max(N0, N1)).
 // kSS (narrow only): the epilogue's thread-private scratch lives in shared
 // memory (after the B stages) instead of per-CTA global memory.
 template <bool kRanged, int kMode, bool kSS = false>
 __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
   constexpr bool kNarrow = kMode >= 1;
   static_assert(kNarrow || !kSS, "shared-memory scratch is narrow-only");
-  constexpr uint32_t kSh = kMode == 2 ? 2u : 0u;  // count scale shift of packed words
+  constexpr uint32_t kSh = kMode >= 2 ? 2u : 0u;  // count scale shift of packed words
   // no-swizzle K-major operand tiles need 16-byte alignment only
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
@@ -440,7 +457,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   if (s.screen) {  // K2 screening table -> shared memory
     const float4* src = reinterpret_cast<const float4*>(d.ktab);
     float4* dst = reinterpret_cast<float4*>(ktab);
-    for (uint32_t x = threadIdx.x; x < d.ktab_n / 4; x += blockDim.x) dst[x] = __ldg(src + x);
+    for (uint32_t x = threadIdx.x; x < s.ktab_n / 4; x += blockDim.x) dst[x] = __ldg(src + x);
   }
   fence_before();
   __syncthreads();
@@ -471,36 +488,51 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     if (lane == 0 && it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
-      uint32_t n = 0, u = 0;
+      // single thread, so every dependent instruction's latency is exposed:
+      // stage / slot indices and phases advance incrementally (no division by
+      // the runtime stage count) and the B descriptors are base + offsets
+      // (the 14-bit address field cannot carry: shared addresses < 256 KiB)
+      uint32_t st = 0, ph = 0, slot = 0, sph = 1;
       const uint32_t tsf = tmem + kSfCol;
+      const uint64_t bdesc0 = f4_desc(smem_u32(stages));
+      long long tl_t0 = tl_clock(), tl_we = 0, tl_wf = 0;
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo& inf = s.info[wk.ii];
 #pragma unroll
         for (uint32_t a = 0; a < 2; ++a) {
 #pragma unroll
-          for (uint32_t c = 0; c < 2; ++c, ++u) {
-            const uint32_t slot = u % kUnits;
-            mbar_wait_a(tempty_s + 8 * slot, ((u / kUnits) & 1) ^ 1);
+          for (uint32_t c = 0; c < 2; ++c) {
+            long long tl_a = tl_clock();
+            mbar_wait_a(tempty_s + 8 * slot, sph);
+            tl_we += tl_clock() - tl_a;
             fence_after();
             const uint32_t nch = inf.q[a][c] / 2;
             const uint32_t dcol = tmem + slot * 128;
-            for (uint32_t ch = 0; ch < nch; ++ch, ++n) {
-              const uint32_t st = n % nst;
-              mbar_wait_spin_a(full_s + 8 * st, (n / nst) & 1);
+            for (uint32_t ch = 0; ch < nch; ++ch) {
+              long long tl_b = tl_clock();
+              mbar_wait_spin_a(full_s + 8 * st, ph);
+              tl_wf += tl_clock() - tl_b;
               fence_after();
               const uint32_t acol = tmem + kACol + st * kAStageCols;
-              const uint32_t bbase = smem_u32(stages + st * kSBStageBytes);
+              const uint64_t bd = bdesc0 + st * uint32_t(kSBStageBytes >> 4);
+              if (!(dbg_skip(s) & 8)) {
 #pragma unroll
-              for (int kk = 0; kk < kSRowBytes / 32; ++kk)
-                mma_f4_ts(dcol, acol + kk * 8, f4_desc(bbase + kk * 256), tsf + sf_col(kk),
-                          (ch != 0 || kk != 0) ? 1u : 0u);
+                for (int kk = 0; kk < kSRowBytes / 32; ++kk)
+                  mma_f4_ts(dcol, acol + kk * 8, bd + kk * (256 >> 4), tsf + sf_col(kk),
+                            (ch != 0 || kk != 0) ? 1u : 0u);
+              }
               mma_commit_a(empty_s + 8 * st);
+              if (++st == nst) { st = 0; ph ^= 1; }
             }
             mma_commit_a(tfull_s + 8 * slot);
+            if (++slot == kUnits) { slot = 0; sph ^= 1; }
           }
         }
         wk.next(s);
       }
+      if (E3_TIMELINE && blockIdx.x < 3)
+        printf("TL cta %d mma: total %lld wait_tempty %lld wait_full %lld tiles %llu\n", blockIdx.x,
+               tl_clock() - tl_t0, tl_we, tl_wf, (unsigned long long)(it1 - it0));
     }
     __syncwarp();
   } else if (warp < kSyrkProducerWarps) {
@@ -517,6 +549,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       SWalker wk;
       wk.start(s, it0);
       uint32_t st = 0, ph = 0;
+      long long tl_t0 = tl_clock(), tl_w = 0;
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo inf = s.info[wk.ii];
         const uint32_t row_a = min(wk.jb * 2 * kJB + r, inf.R - 1);
@@ -536,7 +569,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             y0 = __ldg(Yb + o); y1 = __ldg(Yb + o + R);
           };
           auto stage = [&](uint4 x0, uint4 x1, uint4 y0, uint4 y1) {
+            long long tl_a = tl_clock();
             mbar_wait_a(empty_s + 8 * st, ph ^ 1);
+            tl_w += tl_clock() - tl_a;
             fence_after();  // the MMAs that read this A stage have completed
             if (!(dbg_skip(s) & 2)) {
 #pragma unroll
@@ -554,6 +589,19 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             if (lane == 0) mbar_arrive_a(full_s + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1; }
           };
+#if E3_PF >= 3
+          uint4 a20, a21, b20, b21;
+          if (qtot > 0) load(0, a00, a01, b00, b01);
+          if (qtot > 2) load(2, a10, a11, b10, b11);
+          if (qtot > 4) load(4, a20, a21, b20, b21);
+          for (uint32_t q = 0; q < qtot; q += 2) {
+            const uint4 x0 = a00, x1 = a01, y0 = b00, y1 = b01;
+            a00 = a10; a01 = a11; b00 = b10; b01 = b11;
+            a10 = a20; a11 = a21; b10 = b20; b11 = b21;
+            if (q + 6 < qtot) load(q + 6, a20, a21, b20, b21);
+            stage(x0, x1, y0, y1);
+          }
+#else
           if (qtot > 0) load(0, a00, a01, b00, b01);
           if (qtot > 2) load(2, a10, a11, b10, b11);
           for (uint32_t q = 0; q < qtot; q += 2) {
@@ -562,9 +610,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             if (q + 4 < qtot) load(q + 4, a10, a11, b10, b11);
             stage(x0, x1, y0, y1);
           }
+#endif
         }
         wk.next(s);
       }
+      if (E3_TIMELINE && blockIdx.x < 3 && lane == 0)
+        printf("TL cta %d producer warp %d: total %lld wait_empty %lld\n", blockIdx.x, warp,
+               tl_clock() - tl_t0, tl_w);
     }
   } else if (warp < kMmaWarp) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpilogue));
@@ -606,6 +658,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       else return scr[x * 256];
     };
     uint64_t nevals = 0;
+    long long tl_t0 = tl_clock(), tl_w[2] = {0, 0}, tl_dr = 0, tl_rd = 0;
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
@@ -631,6 +684,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           sjp = __ldg(d.singlep + jc);
           fetch_pairs(0);
         }
+        const long long tl_d0 = tl_clock();
         // ---- drain the four units (a, c) of this tile: TMEM (f32 counts) ->
         // scratch, releasing each ring slot as soon as it is copied, so the MMAs
         // of the next units overlap the scoring below.
@@ -640,8 +694,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
           for (uint32_t a = 0; a < 2; ++a, u += 2) {
             const uint32_t s0 = u % kUnits, s1 = (u + 1) % kUnits;
+            const long long tl_a = tl_clock();
             mbar_wait_a(tfull_s + 8 * s0, (u / kUnits) & 1);
             mbar_wait_a(tfull_s + 8 * s1, ((u + 1) / kUnits) & 1);
+            tl_w[a] += tl_clock() - tl_a;
             fence_after();
             // count c (f32, exact) -> 2^23 + c * 2^kSh by one FFMA (c * 2^kSh < 2^16),
             // then one PRMT joins the low halves of both classes; a class with
@@ -713,6 +769,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             mbar_arrive_a(tempty_s + 8 * slot);
           }
         }
+        const long long tl_d1 = tl_clock();
+        tl_dr += tl_d1 - tl_d0;
         const uint64_t gth = *reinterpret_cast<volatile uint64_t*>(s.gthr);
         // screening bound: a triple whose fp32 screen exceeds thr_f cannot reach
         // the threshold (margin proven on the host, k2_screen_margin)
@@ -812,12 +870,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
                   for (int c = 0; c < 27; ++c) n[c] &= 0x0ffc0ffcu;
                 }
+                if (dbg_skip(s) & 16) {  // profiling: screen lookups within 32 entries (no bank conflicts)
+#pragma unroll
+                  for (int c = 0; c < 27; ++c) n[c] &= 0x007c007cu;
+                }
                 if (dbg_skip(s) & 4)
                   pass[h] = n[26] == 0x7fffffffu;  // profiling: derivation only
                 else
-                  pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled(n, ktab_s, d.st_c1)
+                  pass[h] = valid[h] && (!s.screen || (kSh ? k2_screen_scaled<kMode == 3>(n, ktab_s, d.st_c1)
                                                               : k2_screen_packed(n, ktab_s, d.st_c1)) <= thr_f) &&
-                            !(dbg_skip(s) & 2);
+                            !(dbg_skip(s) & 18);
               }
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
@@ -969,9 +1031,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             }
           }
         }
+        tl_rd += tl_clock() - tl_d1;
         wk.next(s);
       }
     }
+    if (E3_TIMELINE && blockIdx.x < 3 && lane == 0)
+      printf("TL cta %d epilogue warp %d: total %lld drain %lld (wait a0 %lld a1 %lld) rounds %lld\n",
+             blockIdx.x, warp, tl_clock() - tl_t0, tl_dr, tl_w[0], tl_w[1], tl_rd);
     for (uint32_t e = lane; e < nlist; e += 32) s.lists[list * K + e] = make_ulonglong2(ls[e], lt[e]);
     if (lane == 0) s.counts[list] = nlist;
     add_evals(s.evals, nevals);
