@@ -162,13 +162,13 @@ constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-pack
 // A row r — TMEM lane r, so each warp writes its own lane quarter — and B row
 // r), WG1-2 (warps 4-11) run the epilogue, WG3 warp 12 issues the MMAs (13-15
 // idle). setmaxnreg moves registers to the epilogue: per SM sub-partition
-// (one warp of WG0 and of WG3, two of WG1-2) 88 + 2 * 184 + 56 = 512 = the
+// (one warp of WG0 and of WG3, two of WG1-2) 104 + 2 * 176 + 56 = 512 = the
 // 16K-register file / 32 lanes (13 uniform warps were capped at 128 each).
 constexpr int kSyrkProducerWarps = 4;
 constexpr int kSyrkThreads = 32 * 16;
 #ifndef E3_REG_PROD
-#define E3_REG_PROD 88
-#define E3_REG_EPI 184
+#define E3_REG_PROD 104
+#define E3_REG_EPI 176
 #endif
 #ifndef E3_PF
 #define E3_PF 2  // producer: Y quads of this many stages in flight
