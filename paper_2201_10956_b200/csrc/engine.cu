@@ -1590,15 +1590,16 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
       stir ? uint32_t((std::max(ds->N[0], ds->N[1]) + 1 + 3) / 4 * 4) : ds->ktab_n;
   const size_t tab_b = sizeof(float) * ktab_use;
   const size_t cap = ds->smem_optin - 2048;
+  const size_t kst_b = ds->narrow ? size_t(syrk::kKStageTotal) : 0;  // narrow k staging
   uint32_t nst = syrk::kSyrkStages;
   bool screen = !std::getenv("E3_NO_SCREEN");
   if (const char* e = std::getenv("E3_SYRK_STAGES")) nst = uint32_t(std::max(2, std::min(syrk::kSyrkStages, std::atoi(e))));
   if (screen) {
-    while (nst > 2 && 128 + nst * syrk::kSBStageBytes + lists_b + tab_b > cap) --nst;
-    screen = 128 + nst * syrk::kSBStageBytes + lists_b + tab_b <= cap;
+    while (nst > 2 && 128 + nst * syrk::kSBStageBytes + lists_b + tab_b + kst_b > cap) --nst;
+    screen = 128 + nst * syrk::kSBStageBytes + lists_b + tab_b + kst_b <= cap;
     if (!screen) nst = syrk::kSyrkStages;
   }
-  size_t tsm = 128 + nst * syrk::kSBStageBytes + lists_b + (screen ? tab_b : 0);
+  size_t tsm = 128 + nst * syrk::kSBStageBytes + lists_b + (screen ? tab_b : 0) + kst_b;
   // narrow: the epilogue scratch in shared memory when it fits beside the
   // table (two B stages suffice; A lives in TMEM)
   bool sscr = false;
@@ -1606,7 +1607,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     const size_t cap_ss = ds->smem_ss_cap;
     for (uint32_t n2 = nst; n2 >= 2 && !sscr; --n2) {
       const size_t t2 = 128 + n2 * syrk::kSBStageBytes + syrk::kSmemScratchBytes + lists_b +
-                        (screen ? tab_b : 0);
+                        (screen ? tab_b : 0) + kst_b;
       if (t2 <= cap_ss) {
         sscr = true;
         nst = n2;

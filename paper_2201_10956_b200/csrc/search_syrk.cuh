@@ -164,6 +164,21 @@ constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-pack
 // idle). setmaxnreg moves registers to the epilogue: per SM sub-partition
 // (one warp of WG0 and of WG3, two of WG1-2) 104 + 2 * 176 + 56 = 512 = the
 // 16K-register file / 32 lanes (13 uniform warps were capped at 128 each).
+// narrow epilogue: per warp, pair(i, k) and single(k) of its 32 k of the tile
+// staged in shared memory (loaded a tile ahead into registers), so the rounds
+// read them with broadcast LDS instead of global loads that miss the small L1
+constexpr int kKStageBytes = 32 * 16 + 32 * 8;
+constexpr int kKStageTotal = kKStageBytes * 8;   // kEpilogueWarps warps
+__device__ __forceinline__ uint4 lds_u128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
 constexpr int kSyrkProducerWarps = 4;
 constexpr int kSyrkThreads = 32 * 16;
 #ifndef E3_REG_PROD
@@ -174,6 +189,10 @@ constexpr int kSyrkThreads = 32 * 16;
 #define E3_PF 2  // producer: Y quads of this many stages in flight
 #endif
 constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = 56;
+#ifndef E3_ROUND_UNROLL
+#define E3_ROUND_UNROLL 1
+#endif
+constexpr int kRoundUnroll = E3_ROUND_UNROLL;  // narrow epilogue: unroll of the round loop
 static_assert(kRegProducer + 2 * kRegEpilogue + kRegMma <= 512 && kRegProducer % 8 == 0 &&
               kRegEpilogue % 8 == 0, "setmaxnreg budgets");
 constexpr int kEpiWarp0 = 4, kMmaWarp = 12;
@@ -401,6 +420,47 @@ struct SWalker {
   }
 };
 
+// The rare tail of a narrow round, out of line so the hot round loop stays
+// compact in the instruction cache: the exact K2 of the triples whose screen
+// passed, then the warp's top-k offers (warp-synchronous; called by whole
+// warps). Inputs by value (no addressable register arrays on the hot path).
+struct RareIn {
+  uint32_t T[2][8];
+  uint4 pij, pik[2], pjk[2];
+  uint2 sip, sjp, skp[2];
+  uint32_t i, j, kk[2];
+  bool pass[2], valid[2];
+};
+struct RareState {
+  uint32_t nlist;
+  uint64_t lastS, lastT;
+};
+template <uint32_t kSh>
+__device__ __noinline__ RareState syrk_rare(const RareIn in, const double* __restrict__ logp,
+                                            uint32_t npk, uint64_t gth, uint64_t* ls, uint64_t* lt,
+                                            RareState st, uint32_t K, uint64_t* gthr, const Collect col) {
+  const int lane = threadIdx.x & 31;
+  uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    if (in.pass[h]) {
+      uint32_t n[27], n0[27], n1[27];
+      derive_cells(in.T[h], in.pij, in.pik[h], in.pjk[h], in.sip, in.sjp, in.skp[h], npk, n);
+#pragma unroll
+      for (int c = 0; c < 27; ++c) {
+        n0[c] = (n[c] & 0xffffu) >> kSh;
+        n1[c] = n[c] >> (16 + kSh);
+      }
+      sk[h] = score_key(k2_device(n0, n1, logp));
+      tk[h] = triple_key(in.i, in.j, in.kk[h]);
+    }
+  }
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h)
+    offer_cached(in.valid[h], sk[h], tk[h], gth, ls, lt, st.nlist, K, lane, gthr, col, st.lastS, st.lastT);
+  return st;
+}
+
 // kNarrow: every class has < 2^16 samples, so counts are carried as
 // class-packed u16 pairs (class0 | class1 << 16) — scratch, pair index,
 // singles — and the dropped-phase recovery and the table derivation run on
@@ -428,6 +488,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   uint64_t* lists = reinterpret_cast<uint64_t*>(smem + nst * kSBStageBytes +
                                                 (kSS ? kSmemScratchBytes : 0));
   float* ktab = reinterpret_cast<float*>(lists + size_t(kEpilogueWarps) * 2 * s.top_k);
+  // narrow: per-warp k staging (kKStageTotal bytes) after the screening table
+  uint8_t* kstage = reinterpret_cast<uint8_t*>(ktab) + (s.screen ? size_t(s.ktab_n) * 4 : 0);
   __shared__ uint64_t full_bar[kSyrkStages], empty_bar[kSyrkStages];
   __shared__ uint64_t tfull_bar[kUnits], tempty_bar[kUnits];
   __shared__ uint32_t tmem_base_sh;
@@ -659,12 +721,37 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     };
     uint64_t nevals = 0;
     long long tl_t0 = tl_clock(), tl_w[2] = {0, 0}, tl_dr = 0, tl_rd = 0;
+    uint32_t kst_s = smem_u32(kstage + ew * kKStageBytes);
+    asm volatile("" : "+r"(kst_s));
+    // next tile's pair(i, k) / single(k) for k = this warp's 32 k, lane = k
+    uint4 npik = make_uint4(0, 0, 0, 0);
+    uint2 nskp = make_uint2(0, 0);
+    auto load_k = [&](const SWalker& w) {
+      const uint32_t i_ = s.i_lo + w.ii;
+      const uint32_t k_ = min(i_ + 1 + w.kb * kJB + 32 * half + lane, M - 1);
+      npik = __ldg(d.pairp + size_t(i_) * M + k_);
+      nskp = __ldg(d.singlep + k_);
+    };
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
       uint32_t u = 0;
+      if constexpr (kNarrow) load_k(wk);
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo inf = s.info[wk.ii];
+        if constexpr (kNarrow) {
+          __syncwarp();  // the previous tile's rounds are done with the staging
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(kst_s + lane * 16), "r"(npik.x),
+                       "r"(npik.y), "r"(npik.z), "r"(npik.w) : "memory");
+          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(kst_s + 512 + lane * 8), "r"(nskp.x),
+                       "r"(nskp.y) : "memory");
+          __syncwarp();
+          if (it + 1 < it1) {
+            SWalker nw = wk;
+            nw.next(s);
+            load_k(nw);
+          }
+        }
         const uint32_t i = s.i_lo + wk.ii;
         const uint32_t j = i + 1 + wk.jb * kJB + jl;
         const uint32_t jc = min(j, M - 1);
@@ -802,6 +889,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                   Wn[a][t][g] = scr_ld(a * kRounds * 8 + mm * 8 + t * 2 + g);
           };
           fetch_round(0);
+#pragma unroll kRoundUnroll
           for (int m = 0; m < kRounds; ++m) {
             uint4 pjk[2];
             // W[a][t][g]: this row (j, b=bsel), unit slot a, k phase t, genotype g
@@ -836,16 +924,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               }
             }
             nevals += uint32_t(valid[0]) + uint32_t(valid[1]);
-            uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
-            if (valid[0] || valid[1]) {
+            if (__any_sync(0xffffffffu, valid[0] || valid[1])) {
               uint32_t T[2][8];  // [h][a*4 + b*2 + g], class-packed
               uint4 pik[2];
               uint2 skp[2];
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const uint32_t kc = min(kk[h], M - 1);
-                pik[h] = __ldg(d.pairp + size_t(i) * M + kc);
-                skp[h] = __ldg(d.singlep + kc);
+                // this warp's staged k index 4m + 2 bsel + h (clamped like kk)
+                const uint32_t kx = 4 * m + 2 * bsel + h;
+                pik[h] = lds_u128(kst_s + kx * 16);
+                skp[h] = lds_u64(kst_s + 512 + kx * 8);
                 const uint32_t P[4] = {pjk[h].x, pjk[h].y, pjk[h].z, pjk[h].w};
 #pragma unroll
                 for (int b = 0; b < 2; ++b)
@@ -881,24 +969,33 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                                                               : k2_screen_packed(n, ktab_s, d.st_c1)) <= thr_f) &&
                             !(dbg_skip(s) & 18);
               }
+              // rare once the threshold has settled: exact K2 + offers out of
+              // line (a warp none of whose triples passed offers nothing: its
+              // score keys would all be ~0, never inserted or collected)
+              if (__any_sync(0xffffffffu, pass[0] || pass[1])) {
+                RareIn in;
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                if (pass[h]) {  // rare once the threshold has settled: score exactly
-                  uint32_t n[27], n0[27], n1[27];
-                  derive_cells(T[h], pij, pik[h], pjk[h], sip, sjp, skp[h], d.npk, n);
+                for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                  for (int c = 0; c < 27; ++c) {
-                    n0[c] = (n[c] & 0xffffu) >> kSh;
-                    n1[c] = n[c] >> (16 + kSh);
-                  }
-                  sk[h] = score_key(k2_device(n0, n1, d.logp));
-                  tk[h] = triple_key(i, j, kk[h]);
+                  for (int x = 0; x < 8; ++x) in.T[h][x] = T[h][x];
+                  in.pik[h] = pik[h];
+                  in.pjk[h] = pjk[h];
+                  in.skp[h] = skp[h];
+                  in.kk[h] = kk[h];
+                  in.pass[h] = pass[h];
+                  in.valid[h] = valid[h];
                 }
+                in.pij = pij;
+                in.sip = sip;
+                in.sjp = sjp;
+                in.i = i;
+                in.j = j;
+                const RareState r = syrk_rare<kSh>(in, d.logp, d.npk, gth, ls, lt,
+                                                   RareState{nlist, lastS, lastT}, K, s.gthr, s.col);
+                nlist = r.nlist;
+                lastS = r.lastS;
+                lastT = r.lastT;
               }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              offer_cached(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col, lastS, lastT);
             }
           }
         } else {
