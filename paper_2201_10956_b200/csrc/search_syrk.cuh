@@ -193,6 +193,16 @@ constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = 5
 #define E3_ROUND_UNROLL 1
 #endif
 constexpr int kRoundUnroll = E3_ROUND_UNROLL;  // narrow epilogue: unroll of the round loop
+// code size matters (the SM's instruction cache is shared by three warp
+// roles): unroll factors of the MMA issuer's unit (a, c) and stage loops and
+// of the narrow drain's slot loop
+#ifndef E3_MMA_AC_UNROLL
+#define E3_MMA_AC_UNROLL 1
+#define E3_MMA_CH_UNROLL 1
+#define E3_DRAIN_UNROLL 2
+#endif
+constexpr int kMmaAcUnroll = E3_MMA_AC_UNROLL, kMmaChUnroll = E3_MMA_CH_UNROLL,
+              kDrainUnroll = E3_DRAIN_UNROLL;
 static_assert(kRegProducer + 2 * kRegEpilogue + kRegMma <= 512 && kRegProducer % 8 == 0 &&
               kRegEpilogue % 8 == 0, "setmaxnreg budgets");
 constexpr int kEpiWarp0 = 4, kMmaWarp = 12;
@@ -560,9 +570,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       long long tl_t0 = tl_clock(), tl_we = 0, tl_wf = 0;
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo& inf = s.info[wk.ii];
-#pragma unroll
+#pragma unroll kMmaAcUnroll
         for (uint32_t a = 0; a < 2; ++a) {
-#pragma unroll
+#pragma unroll kMmaAcUnroll
           for (uint32_t c = 0; c < 2; ++c) {
             long long tl_a = tl_clock();
             mbar_wait_a(tempty_s + 8 * slot, sph);
@@ -570,6 +580,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             fence_after();
             const uint32_t nch = inf.q[a][c] / 2;
             const uint32_t dcol = tmem + slot * 128;
+#pragma unroll kMmaChUnroll
             for (uint32_t ch = 0; ch < nch; ++ch) {
               long long tl_b = tl_clock();
               mbar_wait_spin_a(full_s + 8 * st, ph);
@@ -778,7 +789,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         if constexpr (kNarrow) {
           // the two classes of slot a are drained together into class-packed
           // words (a, m, t, g) = class0 | class1 << 16
-#pragma unroll
+#pragma unroll kDrainUnroll
           for (uint32_t a = 0; a < 2; ++a, u += 2) {
             const uint32_t s0 = u % kUnits, s1 = (u + 1) % kUnits;
             const long long tl_a = tl_clock();
