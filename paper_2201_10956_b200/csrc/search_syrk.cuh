@@ -70,6 +70,34 @@ __device__ __forceinline__ void mma_f4_ts(uint32_t tmem_d, uint32_t tmem_a, uint
       "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%5], p;\n\t}"
       ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(kIdescF4), "r"(accumulate), "r"(tsf));
 }
+// One stage's four MMAs (K = 4 x 64) and the commit of its operand stage, in
+// one asm block issued by one elected lane of a converged warp: the warp's
+// operands are uniform, so no per-instruction single-lane waterfall is needed.
+__device__ __forceinline__ void mma_stage_f4_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                   uint32_t tsf, uint32_t accumulate, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      ".reg .b32 a1, a2, a3, s1, s2;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u64 b1, %2, 16;\n\tadd.u64 b2, %2, 32;\n\tadd.u64 b3, %2, 48;\n\t"
+      "add.u32 s1, %4, 8;\n\tadd.u32 s2, %4, 16;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %5, [%4], [%4], p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a1], b1, %5, [s1], [s1], t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a2], b2, %5, [s2], [s2], t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a3], b3, %5, [s2], [s2], t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(accumulate), "r"(tsf), "r"(kIdescF4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+      ::"r"(bar) : "memory");
+}
 // One 256-sample stage of an operand row (two 128-sample quads q0, q1) as
 // E2M1 nibbles: eight 16-byte slabs (32 samples = one block-scale K block
 // each). Slab 2t+h holds "part t" of the four words of quad h: the samples
@@ -196,6 +224,9 @@ constexpr int kRoundUnroll = E3_ROUND_UNROLL;  // narrow epilogue: unroll of the
 // code size matters (the SM's instruction cache is shared by three warp
 // roles): unroll factors of the MMA issuer's unit (a, c) and stage loops and
 // of the narrow drain's slot loop
+#ifndef E3_MMA_WARP
+#define E3_MMA_WARP 1  // MMA issuer as a converged warp (elect inside the asm)
+#endif
 #ifndef E3_MMA_AC_UNROLL
 #define E3_MMA_AC_UNROLL 1
 #define E3_MMA_CH_UNROLL 1
@@ -557,10 +588,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   if (warp == kMmaWarp) {
     // ===================== MMA issuer (one thread) =====================
     // Units (tile, a, c) in order; unit u accumulates into ring slot u % kUnits.
-    if (lane == 0 && it0 < it1) {
+    if ((E3_MMA_WARP || lane == 0) && it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
-      // single thread, so every dependent instruction's latency is exposed:
+      // one thread (or a converged warp with E3_MMA_WARP, electing the issuing
+      // lane inside the asm), so every dependent instruction's latency is exposed:
       // stage / slot indices and phases advance incrementally (no division by
       // the runtime stage count) and the B descriptors are base + offsets
       // (the 14-bit address field cannot carry: shared addresses < 256 KiB)
@@ -588,22 +620,29 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               fence_after();
               const uint32_t acol = tmem + kACol + st * kAStageCols;
               const uint64_t bd = bdesc0 + st * uint32_t(kSBStageBytes >> 4);
-              if (!(dbg_skip(s) & 8)) {
+              if (E3_MMA_WARP) {
+                static_assert(kSRowBytes / 32 == 4 && sf_col(1) == 8 && sf_col(2) == 16 && sf_col(3) == 16,
+                              "mma_stage_f4_elect layout");
+                mma_stage_f4_elect(dcol, acol, bd, tsf, ch != 0 ? 1u : 0u, empty_s + 8 * st);
+              } else {
+                if (!(dbg_skip(s) & 8)) {
 #pragma unroll
-                for (int kk = 0; kk < kSRowBytes / 32; ++kk)
-                  mma_f4_ts(dcol, acol + kk * 8, bd + kk * (256 >> 4), tsf + sf_col(kk),
-                            (ch != 0 || kk != 0) ? 1u : 0u);
+                  for (int kk = 0; kk < kSRowBytes / 32; ++kk)
+                    mma_f4_ts(dcol, acol + kk * 8, bd + kk * (256 >> 4), tsf + sf_col(kk),
+                              (ch != 0 || kk != 0) ? 1u : 0u);
+                }
+                mma_commit_a(empty_s + 8 * st);
               }
-              mma_commit_a(empty_s + 8 * st);
               if (++st == nst) { st = 0; ph ^= 1; }
             }
-            mma_commit_a(tfull_s + 8 * slot);
+            if (E3_MMA_WARP) commit_elect(tfull_s + 8 * slot);
+            else mma_commit_a(tfull_s + 8 * slot);
             if (++slot == kUnits) { slot = 0; sph ^= 1; }
           }
         }
         wk.next(s);
       }
-      if (E3_TIMELINE && blockIdx.x < 3)
+      if (E3_TIMELINE && blockIdx.x < 3 && lane == 0)
         printf("TL cta %d mma: total %lld wait_tempty %lld wait_full %lld tiles %llu\n", blockIdx.x,
                tl_clock() - tl_t0, tl_we, tl_wf, (unsigned long long)(it1 - it0));
     }
