@@ -213,9 +213,6 @@ constexpr int kSyrkThreads = 32 * 16;
 #define E3_REG_PROD 104
 #define E3_REG_EPI 176
 #endif
-#ifndef E3_PF
-#define E3_PF 2  // producer: Y quads of this many stages in flight
-#endif
 constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = 56;
 #ifndef E3_ROUND_UNROLL
 #define E3_ROUND_UNROLL 1
@@ -666,19 +663,25 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         const IInfo inf = s.info[wk.ii];
         const uint32_t row_a = min(wk.jb * 2 * kJB + r, inf.R - 1);
         const uint32_t row_b = min(wk.kb * 2 * kJB + r, inf.R - 1);
-#pragma unroll
+#pragma unroll 1
         for (uint32_t a = 0; a < 2; ++a) {
-          const uint4* Ya = s.Y + inf.y_off[a] + row_a;
-          const uint4* Yb = s.Y + inf.y_off[a] + row_b;
+          const uint4* __restrict__ Ya = s.Y + inf.y_off[a] + row_a;
+          const uint4* __restrict__ Yb = s.Y + inf.y_off[a] + row_b;
           const uint32_t R = inf.R;
           const uint32_t qtot = inf.q[a][0] + inf.q[a][1];  // even: 256-sample stages
-          // Y quads of the next two stages in flight (L2 latency). (Unrolling
-          // over stage pairs to avoid the register moves measured -16% at cfg3.)
+          // Y quads of the next two stages in flight (L2 latency): two
+          // register sets, the loop unrolled over stage pairs so the load of
+          // stage q + 2 goes into the set stage q just consumed (register
+          // rotation would wait for the in-flight loads one stage early), with
+          // running row pointers (no per-load 64-bit index arithmetic)
+          const uint32_t nsu = qtot / 2;  // stages of this unit
+          const size_t R2 = size_t(2) * R;
           uint4 a00, a01, b00, b01, a10, a11, b10, b11;
-          auto load = [&](uint32_t q, uint4& x0, uint4& x1, uint4& y0, uint4& y1) {
-            const size_t o = size_t(q) * R;
-            x0 = __ldg(Ya + o); x1 = __ldg(Ya + o + R);
-            y0 = __ldg(Yb + o); y1 = __ldg(Yb + o + R);
+          auto load = [&](uint4& x0, uint4& x1, uint4& y0, uint4& y1) {
+            x0 = __ldg(Ya); x1 = __ldg(Ya + R);
+            y0 = __ldg(Yb); y1 = __ldg(Yb + R);
+            Ya += R2;
+            Yb += R2;
           };
           auto stage = [&](uint4 x0, uint4 x1, uint4 y0, uint4 y1) {
             long long tl_a = tl_clock();
@@ -701,28 +704,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             if (lane == 0) mbar_arrive_a(full_s + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1; }
           };
-#if E3_PF >= 3
-          uint4 a20, a21, b20, b21;
-          if (qtot > 0) load(0, a00, a01, b00, b01);
-          if (qtot > 2) load(2, a10, a11, b10, b11);
-          if (qtot > 4) load(4, a20, a21, b20, b21);
-          for (uint32_t q = 0; q < qtot; q += 2) {
-            const uint4 x0 = a00, x1 = a01, y0 = b00, y1 = b01;
-            a00 = a10; a01 = a11; b00 = b10; b01 = b11;
-            a10 = a20; a11 = a21; b10 = b20; b11 = b21;
-            if (q + 6 < qtot) load(q + 6, a20, a21, b20, b21);
-            stage(x0, x1, y0, y1);
+          if (nsu > 0) load(a00, a01, b00, b01);
+          if (nsu > 1) load(a10, a11, b10, b11);
+          for (uint32_t u2 = 0; u2 < nsu; u2 += 2) {
+            stage(a00, a01, b00, b01);
+            if (u2 + 2 < nsu) load(a00, a01, b00, b01);
+            if (u2 + 1 < nsu) {
+              stage(a10, a11, b10, b11);
+              if (u2 + 3 < nsu) load(a10, a11, b10, b11);
+            }
           }
-#else
-          if (qtot > 0) load(0, a00, a01, b00, b01);
-          if (qtot > 2) load(2, a10, a11, b10, b11);
-          for (uint32_t q = 0; q < qtot; q += 2) {
-            const uint4 x0 = a00, x1 = a01, y0 = b00, y1 = b01;
-            a00 = a10; a01 = a11; b00 = b10; b01 = b11;
-            if (q + 4 < qtot) load(q + 4, a10, a11, b10, b11);
-            stage(x0, x1, y0, y1);
-          }
-#endif
         }
         wk.next(s);
       }
