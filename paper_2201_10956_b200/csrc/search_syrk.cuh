@@ -190,7 +190,7 @@ constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-pack
 // A row r — TMEM lane r, so each warp writes its own lane quarter — and B row
 // r), WG1-2 (warps 4-11) run the epilogue, WG3 warp 12 issues the MMAs (13-15
 // idle). setmaxnreg moves registers to the epilogue: per SM sub-partition
-// (one warp of WG0 and of WG3, two of WG1-2) 104 + 2 * 176 + 56 = 512 = the
+// (one warp of WG0 and of WG3, two of WG1-2) 120 + 2 * 168 + 56 = 512 = the
 // 16K-register file / 32 lanes (13 uniform warps were capped at 128 each).
 // narrow epilogue: per warp, pair(i, k) and single(k) of its 32 k of the tile
 // staged in shared memory (loaded a tile ahead into registers), so the rounds
@@ -210,8 +210,8 @@ __device__ __forceinline__ uint2 lds_u64(uint32_t a) {
 constexpr int kSyrkProducerWarps = 4;
 constexpr int kSyrkThreads = 32 * 16;
 #ifndef E3_REG_PROD
-#define E3_REG_PROD 104
-#define E3_REG_EPI 176
+#define E3_REG_PROD 120
+#define E3_REG_EPI 168
 #endif
 constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = 56;
 #ifndef E3_ROUND_UNROLL

@@ -12,4 +12,5 @@ FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler 
 $NVCC $FL "$@" -c "$ROOT/paper_2201_10956_b200/csrc/engine.cu" -o "$OUT/engine.o"
 $NVCC $FL -c "$ROOT/paper_2201_10956_b200/csrc/host.cpp" -o "$OUT/host.o"
 $NVCC -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libepi3cu.so" "$OUT/engine.o" "$OUT/host.o" -cudart shared
+rm -f "$OUT/engine.o" "$OUT/host.o"  # keep the gpurun snapshot small (< 512 MiB)
 echo "$OUT/libepi3cu.so"
