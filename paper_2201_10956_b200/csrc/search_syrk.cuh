@@ -499,36 +499,6 @@ __device__ __noinline__ RareState syrk_rare(const RareIn in, const double* __res
   return st;
 }
 
-// The wide path's rare tail (per class u32 counts), as syrk_rare.
-struct RareInWide {
-  uint32_t T[2][2][8];
-  uint4 pij[2], pik[2][2], pjk[2][2];
-  uint2 si[2], sj[2], skc[2][2];
-  uint32_t i, j, kk[2];
-  bool pass[2], valid[2];
-};
-__device__ __noinline__ RareState syrk_rare_wide(const RareInWide in, const double* __restrict__ logp,
-                                                 uint32_t n0c, uint32_t n1c, uint64_t gth, uint64_t* ls,
-                                                 uint64_t* lt, RareState st, uint32_t K, uint64_t* gthr,
-                                                 const Collect col) {
-  const int lane = threadIdx.x & 31;
-  uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
-#pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    if (in.pass[h]) {
-      uint32_t n0[27], n1[27];
-      derive_cells(in.T[h][0], in.pij[0], in.pik[h][0], in.pjk[h][0], in.si[0], in.sj[0], in.skc[h][0], n0c, n0);
-      derive_cells(in.T[h][1], in.pij[1], in.pik[h][1], in.pjk[h][1], in.si[1], in.sj[1], in.skc[h][1], n1c, n1);
-      sk[h] = score_key(k2_device(n0, n1, logp));
-      tk[h] = triple_key(in.i, in.j, in.kk[h]);
-    }
-  }
-#pragma unroll 1
-  for (int h = 0; h < 2; ++h)
-    offer_cached(in.valid[h], sk[h], tk[h], gth, ls, lt, st.nlist, K, lane, gthr, col, st.lastS, st.lastT);
-  return st;
-}
-
 // kNarrow: every class has < 2^16 samples, so counts are carried as
 // class-packed u16 pairs (class0 | class1 << 16) — scratch, pair index,
 // singles — and the dropped-phase recovery and the table derivation run on
@@ -1141,7 +1111,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               }
             }
             nevals += uint32_t(valid[0]) + uint32_t(valid[1]);
-            if (__any_sync(0xffffffffu, valid[0] || valid[1])) {
+            uint64_t sk[2] = {~0ull, ~0ull}, tk[2] = {~0ull, ~0ull};
+            if (valid[0] || valid[1]) {
               uint4 pik[2][2];
               uint2 skc[2][2];
   #pragma unroll
@@ -1181,37 +1152,24 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 else
                   pass[h] = valid[h] && (!s.screen || k2_screen(n0, n1, ktab_s) <= thr_f);
               }
-              // rare once the threshold has settled: exact K2 + offers out of line
-              if (__any_sync(0xffffffffu, pass[0] || pass[1])) {
-                RareInWide in;
   #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-  #pragma unroll
-                  for (int c = 0; c < 2; ++c) {
-  #pragma unroll
-                    for (int x = 0; x < 8; ++x) in.T[h][c][x] = T[h][c][x];
-                    in.pik[h][c] = pik[h][c];
-                    in.pjk[h][c] = pjk[h][c];
-                    in.skc[h][c] = skc[h][c];
-                  }
-                  in.kk[h] = kk[h];
-                  in.pass[h] = pass[h];
-                  in.valid[h] = valid[h];
+              for (int h = 0; h < 2; ++h) {
+                if (pass[h]) {  // rare once the threshold has settled: score exactly
+                  uint32_t n0[27], n1[27];
+                  derive_cells(T[h][0], pij0, pik[h][0], pjk[h][0], si0, sj0, skc[h][0], d.n[0], n0);
+                  derive_cells(T[h][1], pij1, pik[h][1], pjk[h][1], si1, sj1, skc[h][1], d.n[1], n1);
+                  sk[h] = score_key(k2_device(n0, n1, d.logp));
+                  tk[h] = triple_key(i, j, kk[h]);
                 }
-                in.pij[0] = pij0; in.pij[1] = pij1;
-                in.si[0] = si0; in.si[1] = si1;
-                in.sj[0] = sj0; in.sj[1] = sj1;
-                in.i = i;
-                in.j = j;
-                const RareState r = syrk_rare_wide(in, d.logp, d.n[0], d.n[1], gth, ls, lt,
-                                                   RareState{nlist, lastS, lastT}, K, s.gthr, s.col);
-                nlist = r.nlist;
-                lastS = r.lastS;
-                lastT = r.lastT;
               }
+            }
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              offer_cached(valid[h], sk[h], tk[h], gth, ls, lt, nlist, K, lane, s.gthr, s.col, lastS, lastT);
             }
           }
         }
+        tl_rd += tl_clock() - tl_d1;
         wk.next(s);
       }
     }
