@@ -1483,9 +1483,26 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     auto c3 = [](uint64_t n) { return n < 3 ? 0 : n * (n - 1) / 2 * (n - 2) / 3; };
     return c3(M) - c3(M - i);
   };
-  // uint4 elements per batch (48 MiB); E3_SYRK_YBUDGET_KIB shrinks it so small
-  // datasets plan many batches (tests of the multi-batch path)
-  const size_t kYBudget = ds->y_budget ? ds->y_budget : size_t(3) << 20;
+  // uint4 elements per batch: 48 MiB (M < 4096: cfg2 loses 4% at 64 MiB),
+  // 64 MiB for M >= 4096, 128 MiB when the operands are also dense in tiles
+  // (<= 3 KiB of Y per 64x64 tile at the first SNP of the search): fewer
+  // launches and batch tails, measured cfg3 483 -> 495 Tel/s, while cfg5
+  // (8.5 KiB per tile) peaks at 64 MiB and loses 6% at 96.
+  // E3_SYRK_YBUDGET_KIB sets it (tests shrink it so small datasets plan many
+  // batches)
+  size_t kYBudget = ds->y_budget ? ds->y_budget : (M >= 4096 ? size_t(4) << 20 : size_t(3) << 20);
+  if (!ds->y_budget && M >= 4096) {
+    size_t ysz0 = 0;
+    for (int c = 0; c < 2; ++c) {
+      const uint2 sc = ds->h_single[c][i_first];
+      const uint64_t g[3] = {sc.x, sc.y, ds->N[c] - sc.x - sc.y};
+      const uint64_t gmax = std::max(g[0], std::max(g[1], g[2]));
+      ysz0 += ((g[0] + 255) / 256 + (g[1] + 255) / 256 + (g[2] + 255) / 256 - (gmax + 255) / 256) * 2;
+    }
+    const double bytes_per_tile = double(ysz0) * 16.0 * double(2 * (M - 1 - i_first)) /
+                                  double(std::max<uint64_t>(1, syrk::tiles_of(M, i_first)));
+    if (bytes_per_tile <= 3072.0) kYBudget = size_t(8) << 20;
+  }
   const size_t kYMax = std::max(kYBudget, size_t(16) << 20);  // hard cap (256 MiB per buffer)
   struct Batch {
     uint32_t first, n, rmax, qmax;

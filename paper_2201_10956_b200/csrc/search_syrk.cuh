@@ -213,7 +213,10 @@ constexpr int kSyrkThreads = 32 * 16;
 #define E3_REG_PROD 120
 #define E3_REG_EPI 168
 #endif
-constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = 56;
+#ifndef E3_REG_MMA
+#define E3_REG_MMA 56
+#endif
+constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = E3_REG_MMA;
 #ifndef E3_ROUND_UNROLL
 #define E3_ROUND_UNROLL 1
 #endif
