@@ -102,15 +102,16 @@ extern "C" int e3_partition(uint64_t M, uint32_t parts, uint64_t* bounds) {
 }
 
 // Cost-balanced partition for the multi-GPU split: the SYRK engine's device
-// time over a range is, to ~1-3% (64-slice profiles of cfg3 and cfg5 on B200,
-// profiles/r02_partition_model.json), a fixed cost per 64x64 (j,k) tile plus
-// a per-first-SNP cost (compaction, batch boundaries) of about kTilesPerSnp
-// tiles. Ranges hold equal shares of that cost; inside a first SNP the cost
+// time over a range is, to ~1-3%, a fixed cost per 64x64 (j,k) tile plus a
+// per-first-SNP cost (compaction, batch boundaries) of about kTilesPerSnp
+// tiles (64: refitted to the 8 equal-cost ranges of the final cfg3 kernel,
+// profiles/r02e_bench_cfg3_driver_cmd.json partition_balance; the earlier
+// kernel fitted 16, profiles/r02_partition_model.json). Ranges hold equal shares of that cost; inside a first SNP the cost
 // is taken as proportional to its triples (j-major order covers tile rows).
 extern "C" int e3_partition_balanced(uint64_t M, uint32_t parts, uint64_t* bounds) {
   if (parts < 1) return fail(E3_DOMAIN, "parts must be >= 1");
   if (M < 3) return fail(E3_DIMENSION, "search needs at least 3 SNPs");
-  constexpr double kTilesPerSnp = 16.0;
+  constexpr double kTilesPerSnp = 64.0;
   constexpr uint64_t kEdge = 64;
   std::vector<double> cw(M - 1, 0.0);  // cumulative cost before first SNP i
   for (uint64_t i = 0; i + 2 < M; ++i) {

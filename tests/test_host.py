@@ -190,7 +190,7 @@ def test_oracle_built_bench_sample_equals_product_input():
 @pytest.mark.parametrize("parts", [1, 2, 3, 4, 8, 16])
 def test_partition_balanced_tiles_the_rank_space(M, parts):
     """e3_partition_balanced: contiguous, ordered ranges covering [0, C(M,3))
-    exactly; on large M the per-range cost model (64x64 tiles + 16 per first
+    exactly; on large M the per-range cost model (64x64 tiles + 64 per first
     SNP) is equal to within a fraction of a first SNP."""
     import numpy as np
     b = epi3.partition_balanced(M, parts)
@@ -201,7 +201,7 @@ def test_partition_balanced_tiles_the_rank_space(M, parts):
     if M >= 2048:
         i = np.arange(M - 2)
         nb = (M - 1 - i + 63) // 64
-        w = nb * (nb + 1) / 2 + 16.0
+        w = nb * (nb + 1) / 2 + 64.0
         tri = (M - 1 - i) * (M - 2 - i) / 2
         ctri = np.concatenate([[0], np.cumsum(tri)])
         costs = []
