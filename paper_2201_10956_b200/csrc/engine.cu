@@ -1523,7 +1523,6 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
       syrk::IInfo inf{};
       inf.R = uint32_t(2 * (M - 1 - i));
       inf.nb = uint32_t((M - 1 - i + syrk::kJB - 1) / syrk::kJB);
-      inf.nkb = uint32_t((M - 1 - i + syrk::kKB - 1) / syrk::kKB);
       size_t ysz = 0;
       for (int c = 0; c < 2; ++c) {
         // genotype counts of SNP i in class c; the largest phase is dropped

@@ -26,16 +26,7 @@ namespace syrk {
 
 using namespace tc;
 
-constexpr int kJB = 64;           // SNPs per j block -> 128 A rows (M = 128)
-// SNPs per k block -> 2 kKB B rows (N = 2 kKB). 48 makes an accumulator unit
-// 96 TMEM columns, so the ring holds a whole tile's four units (the MMAs of
-// tile t+1 then never wait for tile t's drain); 64 is the square tile.
-#ifndef E3_KB
-#define E3_KB 64
-#endif
-constexpr int kKB = E3_KB;
-static_assert(kKB == 64 || kKB == 48, "k block");
-constexpr int kNU = 2 * kKB;      // columns of one (tile, slot, class) accumulator unit
+constexpr int kJB = 64;           // SNPs per j / k block -> 128 operand rows each
 // Operands are packed E2M1 (fp4, two samples per byte; a one is a single-bit
 // nibble whose value the UE8M0 block scale brings back to 1.0, see
 // expand_stage_regs), multiplied by tcgen05.mma kind::mxf4 with f32
@@ -48,19 +39,16 @@ constexpr int kSRowBytes = kSChunk / 2;                // 128 B per operand row
 // 83.5 cycles vs 127.6 with both operands in shared memory,
 // tools/mxf4_ts_probe.cu) — and B (the k rows) in shared memory.
 constexpr int kSyrkStages = 3;                          // a launch uses s.nst of them
-constexpr int kSBStageBytes = kNU * kSRowBytes;       // B only = 16 KiB (12 KiB at kKB 48)
+constexpr int kSBStageBytes = kRows * kSRowBytes;      // B only = 16 KiB
 constexpr uint32_t kAStageCols = kSRowBytes / 4;       // 32 TMEM columns per A stage
 constexpr uint32_t kACol = 416;                        // A stages: columns [416, 512)
-constexpr int kUnits = kKB == 48 ? 4 : 3;  // TMEM ring of (tile, a, c) accumulators, kNU columns each
+constexpr int kUnits = 3;          // TMEM ring of (tile, a, c) accumulators, 128 columns each
 constexpr uint32_t kSfCol = 384;   // scale-factor columns (init_scale_factors)
-static_assert(kACol >= kSfCol + 32 && kACol + kSyrkStages * kAStageCols <= 512 && kUnits * kNU <= kSfCol,
-              "TMEM columns");
+static_assert(kACol >= kSfCol + 32 && kACol + kSyrkStages * kAStageCols <= 512, "TMEM columns");
 constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10)          // A, B = E2M1
                             | (uint32_t(128 >> 3) << 17)      // N = 128
                             | (1u << 23)                      // scale type UE8M0
                             | (uint32_t(128 >> 4) << 24);     // M = 128, K = 64
-// the search kernel's MMAs: N = kNU (the pair-index kernel keeps kIdescF4)
-constexpr uint32_t kIdescSearch = (kIdescF4 & ~(0x3Fu << 17)) | (uint32_t(kNU >> 3) << 17);
 
 // K-major no-swizzle descriptor for a 128-byte stage row (8 16-byte slabs).
 __device__ __forceinline__ uint64_t f4_desc(uint32_t saddr) {
@@ -80,7 +68,7 @@ __device__ __forceinline__ void mma_f4_ts(uint32_t tmem_d, uint32_t tmem_a, uint
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%5], p;\n\t}"
-      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(kIdescSearch), "r"(accumulate), "r"(tsf));
+      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(kIdescF4), "r"(accumulate), "r"(tsf));
 }
 // One stage's four MMAs (K = 4 x 64) and the commit of its operand stage, in
 // one asm block issued by one elected lane of a converged warp: the warp's
@@ -101,7 +89,7 @@ __device__ __forceinline__ void mma_stage_f4_elect(uint32_t tmem_d, uint32_t tme
       "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a2], b2, %5, [s2], [s2], t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a3], b3, %5, [s2], [s2], t;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
-      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(accumulate), "r"(tsf), "r"(kIdescSearch), "r"(bar)
+      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(accumulate), "r"(tsf), "r"(kIdescF4), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void commit_elect(uint32_t bar) {
@@ -195,9 +183,9 @@ __device__ __forceinline__ void expand_stage_f4(uint32_t row_saddr, uint4 q0, ui
                    "r"(f4_part(w[h][3], t))
                    : "memory");
 }
-constexpr int kRounds = kKB / 8;  // 4-k rounds per epilogue warpgroup (kKB / 2 k)
+constexpr int kRounds = 8;        // 4-column rounds per epilogue warpgroup (32 k)
 constexpr int kScratchPerThread = kRounds * 32;  // u32: 8 values x 2 classes x 2 phases per round
-constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-packed, 128 KiB (96 at kKB 48)
+constexpr int kSmemScratchBytes = kRounds * 16 * 256 * 4;  // narrow: class-packed, 128 KiB
 // 16 warps = four warpgroups: WG0 (warps 0-3) expand operands (thread r owns
 // A row r — TMEM lane r, so each warp writes its own lane quarter — and B row
 // r), WG1-2 (warps 4-11) run the epilogue, WG3 warp 12 issues the MMAs (13-15
@@ -259,8 +247,7 @@ struct IInfo {
   uint32_t n[2][2];      // |S_{i,phase(p,c),c}|
   uint32_t q[2][2];      // quads of class c in Y_{i,p} (even: 256-sample stages)
   uint32_t R;            // rows = 2 (M - 1 - i)
-  uint32_t nb;           // j blocks (kJB SNPs) above i
-  uint32_t nkb;          // k blocks (kKB SNPs) above i
+  uint32_t nb;           // 64-SNP blocks above i
   uint32_t drop[2];      // dropped phase per class (slots hold the other two, ascending)
 };
 
@@ -447,11 +434,8 @@ __global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, cons
 }
 
 // Tile walk within a batch: (i, jb, kb) with jb <= kb < nb(i).
-// first k block of j block jb: tile (jb, kb) holds a pair j < k iff
-// kKB (kb + 1) > kJB jb
-__host__ __device__ constexpr uint32_t kb_first(uint32_t jb) { return uint32_t(kJB) * jb / uint32_t(kKB); }
 struct SWalker {
-  uint32_t ii, jb, kb, nb, nkb;
+  uint32_t ii, jb, kb, nb;
   __device__ void start(const SyrkArgs& s, uint64_t item) {
     uint32_t lo = 0, hi = s.n_i - 1;
     while (lo < hi) {
@@ -460,23 +444,19 @@ struct SWalker {
     }
     ii = lo;
     nb = s.info[ii].nb;
-    nkb = s.info[ii].nkb;
     uint64_t u = item - s.itemoff[ii];
     jb = 0;
-    while (u >= uint64_t(nkb - kb_first(jb))) { u -= nkb - kb_first(jb); ++jb; }
-    kb = kb_first(jb) + uint32_t(u);
+    while (u >= uint64_t(nb - jb)) { u -= nb - jb; ++jb; }
+    kb = jb + uint32_t(u);
   }
   __device__ void next(const SyrkArgs& s) {
-    if (++kb == nkb) {
+    if (++kb == nb) {
       if (++jb == nb) {
         ++ii;
         jb = 0;
-        if (ii < s.n_i) {
-          nb = s.info[ii].nb;
-          nkb = s.info[ii].nkb;
-        }
+        if (ii < s.n_i) nb = s.info[ii].nb;
       }
-      kb = kb_first(jb);
+      kb = jb;
     }
   }
 };
@@ -631,7 +611,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             tl_we += tl_clock() - tl_a;
             fence_after();
             const uint32_t nch = inf.q[a][c] / 2;
-            const uint32_t dcol = tmem + slot * kNU;
+            const uint32_t dcol = tmem + slot * 128;
 #pragma unroll kMmaChUnroll
             for (uint32_t ch = 0; ch < nch; ++ch) {
               long long tl_b = tl_clock();
@@ -677,7 +657,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     const uint32_t row_off = (r >> 3) * (kSRowBytes / 16) * 128 + (r & 7) * 16;
     const uint32_t stage_b = smem_u32(stages) + row_off;
     const uint32_t tmem_a = tmem + (uint32_t((warp & 3) * 32) << 16) + kACol;
-    const bool has_b = r < kNU;                 // B has kNU rows (warp-uniform)
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
@@ -686,7 +665,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo inf = s.info[wk.ii];
         const uint32_t row_a = min(wk.jb * 2 * kJB + r, inf.R - 1);
-        const uint32_t row_b = min(wk.kb * 2 * kKB + r, inf.R - 1);
+        const uint32_t row_b = min(wk.kb * 2 * kJB + r, inf.R - 1);
 #pragma unroll 1
         for (uint32_t a = 0; a < 2; ++a) {
           const uint4* __restrict__ Ya = s.Y + inf.y_off[a] + row_a;
@@ -703,9 +682,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           uint4 a00, a01, b00, b01, a10, a11, b10, b11;
           auto load = [&](uint4& x0, uint4& x1, uint4& y0, uint4& y1) {
             x0 = __ldg(Ya); x1 = __ldg(Ya + R);
-            if (has_b) {
-              y0 = __ldg(Yb); y1 = __ldg(Yb + R);
-            }
+            y0 = __ldg(Yb); y1 = __ldg(Yb + R);
             Ya += R2;
             Yb += R2;
           };
@@ -721,7 +698,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 expand_stage_regs(av, x0, x1, hf);
                 tmem_st16(tmem_a + st * kAStageCols + 16 * hf, av);
               }
-              if (has_b) expand_stage_f4(stage_b + st * kSBStageBytes, y0, y1);
+              expand_stage_f4(stage_b + st * kSBStageBytes, y0, y1);
               asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
             fence_before();
@@ -795,7 +772,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     uint2 nskp = make_uint2(0, 0);
     auto load_k = [&](const SWalker& w) {
       const uint32_t i_ = s.i_lo + w.ii;
-      const uint32_t k_ = min(i_ + 1 + w.kb * kKB + (kKB / 2) * half + lane, M - 1);
+      const uint32_t k_ = min(i_ + 1 + w.kb * kJB + 32 * half + lane, M - 1);
       npik = __ldg(d.pairp + size_t(i_) * M + k_);
       nskp = __ldg(d.singlep + k_);
     };
@@ -822,7 +799,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
         const uint32_t i = s.i_lo + wk.ii;
         const uint32_t j = i + 1 + wk.jb * kJB + jl;
         const uint32_t jc = min(j, M - 1);
-        const uint32_t kbase = i + 1 + wk.kb * kKB + 4 * half * kRounds + 2 * bsel;
+        const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
         // narrow: the tile's marginals and round 0's pair(j,k) entries are
         // requested before the drain waits for the MMAs (DRAM latency hidden)
         uint4 pij = make_uint4(0, 0, 0, 0), pjn[2];
@@ -864,8 +841,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 #pragma unroll
               for (int m2 = 0; m2 < kRounds; m2 += 2) {
                 uint32_t v0[16], v1[16];
-                tmem_ld16(tbase + s0 * kNU + 8 * m2, v0);
-                tmem_ld16(tbase + s1 * kNU + 8 * m2, v1);
+                tmem_ld16(tbase + s0 * 128 + 8 * m2, v0);
+                tmem_ld16(tbase + s1 * 128 + 8 * m2, v1);
                 tmem_wait_ld();
                 uint32_t w0[16], w1[16];  // 2^23 + c * 2^kSh, two counts per FFMA2
 #pragma unroll
@@ -906,7 +883,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             fence_after();
             const bool nonempty = inf.q[a][c] != 0;
             const uint32_t taddr =
-                tmem + (uint32_t(quarter * 32) << 16) + slot * kNU + half * 8 * kRounds;
+                tmem + (uint32_t(quarter * 32) << 16) + slot * 128 + half * 8 * kRounds;
 #pragma unroll
             for (int m2 = 0; m2 < kRounds; m2 += 2) {
               uint32_t v[16];
@@ -1129,7 +1106,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             bool valid[2];
   #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              kk[h] = i + 1 + wk.kb * kKB + 4 * (half * kRounds + m) + 2 * bsel + h;
+              kk[h] = i + 1 + wk.kb * kJB + 4 * (half * kRounds + m) + 2 * bsel + h;
               valid[h] = j < kk[h] && kk[h] < M && !(dbg_skip(s) & 1);
               if (kRanged && valid[h]) {
                 const uint64_t rr = rank_ij + (kk[h] - j - 1);
@@ -1215,11 +1192,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
 }
 
 inline uint64_t tiles_of(uint64_t M, uint64_t i) {
-  const uint64_t n = M - 1 - i;
-  const uint64_t nb = (n + kJB - 1) / kJB, nkb = (n + kKB - 1) / kKB;
-  uint64_t t = 0;
-  for (uint64_t jb = 0; jb < nb; ++jb) t += nkb - kb_first(uint32_t(jb));
-  return t;
+  const uint64_t nb = (M - 1 - i + kJB - 1) / kJB;
+  return nb * (nb + 1) / 2;
 }
 
 }  // namespace syrk
