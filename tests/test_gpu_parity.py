@@ -224,13 +224,17 @@ def test_class_beyond_exact_f32_range():
 @pytest.mark.parametrize("env", [{}, {"E3_NO_NARROW": "1"}, {"E3_NO_SCREEN": "1"}, {"E3_NO_SCALED": "1"},
                                  {"E3_SYRK_STAGES": "2"}, {"E3_SYRK_NO_DROP": "1"},
                                  {"E3_NO_SMEM_SCRATCH": "1"}, {"E3_NO_SCALED": "1", "E3_NO_SMEM_SCRATCH": "1"},
-                                 {"E3_NO_NARROW": "1", "E3_NO_SCREEN": "1"}])
-@pytest.mark.parametrize("M,n0,n1,seed", [(48, 700, 333, 21), (20, 20000, 9000, 22)])
+                                 {"E3_NO_NARROW": "1", "E3_NO_SCREEN": "1"},
+                                 {"E3_SCREEN_STIRLING": "1"}, {"E3_SCREEN_STIRLING": "0"}])
+@pytest.mark.parametrize("M,n0,n1,seed", [(48, 700, 333, 21), (20, 20000, 9000, 22),
+                                          (40, 5000, 4200, 23)])
 def test_syrk_code_paths_match_oracle(monkeypatch, env, M, n0, n1, seed):
     """Every SYRK code path (narrow class-packed / wide, screened / exact,
-    fewer operand stages, no dropped phase, epilogue scratch in shared or
-    global memory; segmented compaction for the 20000-sample class) returns
-    the oracle's top-k bit for bit."""
+    the scaled screen's pooled term from the table or from Stirling's bound
+    (automatic for classes >= 4096 samples: the 5000/4200 set), fewer operand
+    stages, no dropped phase, epilogue scratch in shared or global memory;
+    segmented compaction for the 20000-sample class) returns the oracle's
+    top-k bit for bit."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     ds = _random_ds(M, n0, n1, seed)
