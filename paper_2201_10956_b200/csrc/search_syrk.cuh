@@ -45,11 +45,23 @@ constexpr uint32_t kACol = 416;                        // A stages: columns [416
 constexpr int kUnits = 3;          // TMEM ring of (tile, a, c) accumulators, 128 columns each
 constexpr uint32_t kSfCol = 384;   // scale-factor columns (init_scale_factors)
 static_assert(kACol >= kSfCol + 32 && kACol + kSyrkStages * kAStageCols <= 512, "TMEM columns");
+// E3_PAIR: CTA pairs (cta_group::2). The pair's two CTAs take j blocks 2p
+// and 2p + 1 of the same (i, k block): one M256 N128 MMA per K step (issued by
+// the leader, A from each CTA's TMEM, B split over the pair's shared memory:
+// each CTA expands 64 of the 128 B rows), so each SM expands half the B
+// operand and the tensor core runs at 64 instead of 83.5 cycles per
+// M128-equivalent K64 MMA (tools/mxf4_2cta_probe.cu).
+#ifndef E3_PAIR
+#define E3_PAIR 0
+#endif
+constexpr bool kPair = E3_PAIR != 0;
 constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10)          // A, B = E2M1
                             | (uint32_t(128 >> 3) << 17)      // N = 128
                             | (1u << 23)                      // scale type UE8M0
                             | (uint32_t(128 >> 4) << 24);     // M = 128, K = 64
 
+// the pair MMA: M = 256 (each CTA's 128 A rows)
+constexpr uint32_t kIdescPair = (kIdescF4 & ~(0x1Fu << 24)) | (uint32_t(256 >> 4) << 24);
 // K-major no-swizzle descriptor for a 128-byte stage row (8 16-byte slabs).
 __device__ __forceinline__ uint64_t f4_desc(uint32_t saddr) {
   return uint64_t((saddr >> 4) & 0x3fff) | (uint64_t(128 >> 4) << 16) |
@@ -91,6 +103,43 @@ __device__ __forceinline__ void mma_stage_f4_elect(uint32_t tmem_d, uint32_t tme
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}"
       ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(accumulate), "r"(tsf), "r"(kIdescF4), "r"(bar)
       : "memory");
+}
+// the pair's stage: four M256 MMAs (leader CTA), commit multicast to both CTAs
+__device__ __forceinline__ void mma_stage_pair_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                     uint32_t tsf, uint32_t accumulate, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      ".reg .b32 a1, a2, a3, s1, s2;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u64 b1, %2, 16;\n\tadd.u64 b2, %2, 32;\n\tadd.u64 b3, %2, 48;\n\t"
+      "add.u32 s1, %4, 8;\n\tadd.u32 s2, %4, 16;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [%1], %2, %5, [%4], [%4], p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [a1], b1, %5, [s1], [s1], t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [a2], b2, %5, [s2], [s2], t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [a3], b3, %5, [s2], [s2], t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], %7;\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(accumulate), "r"(tsf), "r"(kIdescPair), "r"(bar),
+        "h"((unsigned short)3)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+      ::"r"(bar), "h"((unsigned short)3) : "memory");
+}
+// arrive on the pair leader's (rank 0) copy of a barrier at CTA-local address
+// `bar` (release at cluster scope: the data written before it is visible)
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(bar));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void commit_elect(uint32_t bar) {
   asm volatile(
@@ -434,6 +483,10 @@ __global__ void __launch_bounds__(128) compact_pext_kernel(const DevData d, cons
 }
 
 // Tile walk within a batch: (i, jb, kb) with jb <= kb < nb(i).
+// Tile walk within a batch: (i, jb, kb), kb >= kb_first(jb); with kPair jb
+// indexes pairs of j blocks (2 jb, 2 jb + 1) whose tiles share the k block.
+__host__ __device__ constexpr uint32_t n_jb(uint32_t nb) { return kPair ? (nb + 1) / 2 : nb; }
+__host__ __device__ constexpr uint32_t kb_first(uint32_t jb) { return kPair ? 2 * jb : jb; }
 struct SWalker {
   uint32_t ii, jb, kb, nb;
   __device__ void start(const SyrkArgs& s, uint64_t item) {
@@ -446,17 +499,17 @@ struct SWalker {
     nb = s.info[ii].nb;
     uint64_t u = item - s.itemoff[ii];
     jb = 0;
-    while (u >= uint64_t(nb - jb)) { u -= nb - jb; ++jb; }
-    kb = jb + uint32_t(u);
+    while (u >= uint64_t(nb - kb_first(jb))) { u -= nb - kb_first(jb); ++jb; }
+    kb = kb_first(jb) + uint32_t(u);
   }
   __device__ void next(const SyrkArgs& s) {
     if (++kb == nb) {
-      if (++jb == nb) {
+      if (++jb == n_jb(nb)) {
         ++ii;
         jb = 0;
         if (ii < s.n_i) nb = s.info[ii].nb;
       }
-      kb = jb;
+      kb = kb_first(jb);
     }
   }
 };
@@ -514,8 +567,14 @@ __device__ __noinline__ RareState syrk_rare(const RareIn in, const double* __res
 // shared memory then ends at max(N0, N1)).
 // kSS (narrow only): the epilogue's thread-private scratch lives in shared
 // memory (after the B stages) instead of per-CTA global memory.
+#if E3_PAIR
+#define E3_SYRK_CLUSTER __cluster_dims__(2, 1, 1)
+#else
+#define E3_SYRK_CLUSTER
+#endif
 template <bool kRanged, int kMode, bool kSS = false>
-__global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevData d, const SyrkArgs s) {
+__global__ void E3_SYRK_CLUSTER __launch_bounds__(kSyrkThreads, 1)
+search_syrk_kernel(const DevData d, const SyrkArgs s) {
   constexpr bool kNarrow = kMode >= 1;
   static_assert(kNarrow || !kSS, "shared-memory scratch is narrow-only");
   constexpr uint32_t kSh = kMode >= 2 ? 2u : 0u;  // count scale shift of packed words
@@ -538,24 +597,35 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t M = d.M;
   const uint32_t K = s.top_k;
-  const uint64_t it0 = s.item_begin + s.item_count * blockIdx.x / gridDim.x;
-  const uint64_t it1 = s.item_begin + s.item_count * (blockIdx.x + 1) / gridDim.x;
+  // kPair: the two CTAs of a cluster walk the same items (crank = which j block)
+  uint32_t crank = 0;
+  if constexpr (kPair) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const uint32_t nclus = kPair ? gridDim.x / 2 : gridDim.x, cidx = kPair ? blockIdx.x / 2 : blockIdx.x;
+  const uint64_t it0 = s.item_begin + s.item_count * cidx / nclus;
+  const uint64_t it1 = s.item_begin + s.item_count * (cidx + 1) / nclus;
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < kSyrkStages; ++st) {
-      mbar_init(&full_bar[st], kSyrkProducerWarps);
+      // kPair: the leader's barriers also count one forwarded arrival from the peer
+      mbar_init(&full_bar[st], kSyrkProducerWarps + (kPair && crank == 0 ? 1 : 0));
       mbar_init(&empty_bar[st], 1);
     }
     for (int b = 0; b < kUnits; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 32 * kEpilogueWarps);
+      mbar_init(&tempty_bar[b], kPair ? kEpilogueWarps + (crank == 0 ? 1 : 0) : 32 * kEpilogueWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base_sh)), "n"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base_sh)), "n"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base_sh)), "n"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (s.screen) {  // K2 screening table -> shared memory
     const float4* src = reinterpret_cast<const float4*>(d.ktab);
@@ -563,7 +633,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     for (uint32_t x = threadIdx.x; x < s.ktab_n / 4; x += blockDim.x) dst[x] = __ldg(src + x);
   }
   fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync();  // the peer's barriers exist before any remote arrival
+  else __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base_sh;
   uint32_t ktab_s = smem_u32(ktab);
@@ -588,6 +659,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
   if (warp == kMmaWarp) {
     // ===================== MMA issuer (one thread) =====================
     // Units (tile, a, c) in order; unit u accumulates into ring slot u % kUnits.
+    // kPair: the peer CTA's warp 12 forwards its producers' and epilogue's
+    // local barrier completions to the leader, one cluster-scope arrival each
+    // (producer warps arriving remotely themselves paid a cluster release per
+    // stage that waited for their in-flight prefetch loads: 44% slower)
     if ((E3_MMA_WARP || lane == 0) && it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
@@ -597,6 +672,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       // the runtime stage count) and the B descriptors are base + offsets
       // (the 14-bit address field cannot carry: shared addresses < 256 KiB)
       uint32_t st = 0, ph = 0, slot = 0, sph = 1;
+      uint32_t fwd_units = 0;  // kPair forwarder: units seen
       const uint32_t tsf = tmem + kSfCol;
       const uint64_t bdesc0 = f4_desc(smem_u32(stages));
       long long tl_t0 = tl_clock(), tl_we = 0, tl_wf = 0;
@@ -611,6 +687,18 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             tl_we += tl_clock() - tl_a;
             fence_after();
             const uint32_t nch = inf.q[a][c] / 2;
+            if (kPair && crank != 0) {  // forwarder: the unit's release, then its stages
+              // (the first kUnits waits pass on the initially free slots: nothing to forward)
+              if (lane == 0 && fwd_units >= uint32_t(kUnits)) mbar_arrive_leader(tempty_s + 8 * slot);
+              ++fwd_units;
+              for (uint32_t ch = 0; ch < nch; ++ch) {
+                mbar_wait_spin_a(full_s + 8 * st, ph);
+                if (lane == 0) mbar_arrive_leader(full_s + 8 * st);
+                if (++st == nst) { st = 0; ph ^= 1; }
+              }
+              if (++slot == kUnits) { slot = 0; sph ^= 1; }
+              continue;
+            }
             const uint32_t dcol = tmem + slot * 128;
 #pragma unroll kMmaChUnroll
             for (uint32_t ch = 0; ch < nch; ++ch) {
@@ -620,9 +708,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               fence_after();
               const uint32_t acol = tmem + kACol + st * kAStageCols;
               const uint64_t bd = bdesc0 + st * uint32_t(kSBStageBytes >> 4);
-              if (E3_MMA_WARP) {
-                static_assert(kSRowBytes / 32 == 4 && sf_col(1) == 8 && sf_col(2) == 16 && sf_col(3) == 16,
-                              "mma_stage_f4_elect layout");
+              static_assert(kSRowBytes / 32 == 4 && sf_col(1) == 8 && sf_col(2) == 16 && sf_col(3) == 16,
+                            "mma_stage_f4_elect layout");
+              if (kPair) {
+                mma_stage_pair_elect(dcol, acol, bd, tsf, ch != 0 ? 1u : 0u, empty_s + 8 * st);
+              } else if (E3_MMA_WARP) {
                 mma_stage_f4_elect(dcol, acol, bd, tsf, ch != 0 ? 1u : 0u, empty_s + 8 * st);
               } else {
                 if (!(dbg_skip(s) & 8)) {
@@ -635,7 +725,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               }
               if (++st == nst) { st = 0; ph ^= 1; }
             }
-            if (E3_MMA_WARP) commit_elect(tfull_s + 8 * slot);
+            if (kPair) commit_pair_elect(tfull_s + 8 * slot);
+            else if (E3_MMA_WARP) commit_elect(tfull_s + 8 * slot);
             else mma_commit_a(tfull_s + 8 * slot);
             if (++slot == kUnits) { slot = 0; sph ^= 1; }
           }
@@ -657,6 +748,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     const uint32_t row_off = (r >> 3) * (kSRowBytes / 16) * 128 + (r & 7) * 16;
     const uint32_t stage_b = smem_u32(stages) + row_off;
     const uint32_t tmem_a = tmem + (uint32_t((warp & 3) * 32) << 16) + kACol;
+    const bool has_b = !kPair || r < 64;        // kPair: each CTA expands 64 B rows (warp-uniform)
     if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
@@ -664,8 +756,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
       long long tl_t0 = tl_clock(), tl_w = 0;
       for (uint64_t it = it0; it < it1; ++it) {
         const IInfo inf = s.info[wk.ii];
-        const uint32_t row_a = min(wk.jb * 2 * kJB + r, inf.R - 1);
-        const uint32_t row_b = min(wk.kb * 2 * kJB + r, inf.R - 1);
+        // kPair: this CTA's j block of the pair; its half (64 rows) of the B rows
+        const uint32_t jbx = kPair ? 2 * wk.jb + crank : wk.jb;
+        const uint32_t row_a = min(jbx * 2 * kJB + r, inf.R - 1);
+        const uint32_t row_b = min(wk.kb * 2 * kJB + (kPair ? 64 * crank : 0u) + r, inf.R - 1);
 #pragma unroll 1
         for (uint32_t a = 0; a < 2; ++a) {
           const uint4* __restrict__ Ya = s.Y + inf.y_off[a] + row_a;
@@ -682,7 +776,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           uint4 a00, a01, b00, b01, a10, a11, b10, b11;
           auto load = [&](uint4& x0, uint4& x1, uint4& y0, uint4& y1) {
             x0 = __ldg(Ya); x1 = __ldg(Ya + R);
-            y0 = __ldg(Yb); y1 = __ldg(Yb + R);
+            if (has_b) {
+              y0 = __ldg(Yb); y1 = __ldg(Yb + R);
+            }
             Ya += R2;
             Yb += R2;
           };
@@ -698,7 +794,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
                 expand_stage_regs(av, x0, x1, hf);
                 tmem_st16(tmem_a + st * kAStageCols + 16 * hf, av);
               }
-              expand_stage_f4(stage_b + st * kSBStageBytes, y0, y1);
+              if (has_b) expand_stage_f4(stage_b + st * kSBStageBytes, y0, y1);
               asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
             fence_before();
@@ -797,7 +893,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
           }
         }
         const uint32_t i = s.i_lo + wk.ii;
-        const uint32_t j = i + 1 + wk.jb * kJB + jl;
+        const uint32_t j = i + 1 + (kPair ? 2 * wk.jb + crank : wk.jb) * kJB + jl;
         const uint32_t jc = min(j, M - 1);
         const uint32_t kbase = i + 1 + wk.kb * kJB + 4 * half * kRounds + 2 * bsel;
         // narrow: the tile's marginals and round 0's pair(j,k) entries are
@@ -870,8 +966,16 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
             if (e0 || e1) drain(std::true_type{});
             else drain(std::false_type{});
             fence_before();
-            mbar_arrive_a(tempty_s + 8 * s0);
-            mbar_arrive_a(tempty_s + 8 * s1);
+            if constexpr (kPair) {  // one arrival per warp (the peer forwards its own)
+              __syncwarp();
+              if (lane == 0) {
+                mbar_arrive_a(tempty_s + 8 * s0);
+                mbar_arrive_a(tempty_s + 8 * s1);
+              }
+            } else {
+              mbar_arrive_a(tempty_s + 8 * s0);
+              mbar_arrive_a(tempty_s + 8 * s1);
+            }
           }
         } else {
 #pragma unroll
@@ -897,7 +1001,12 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
               }
             }
             fence_before();
-            mbar_arrive_a(tempty_s + 8 * slot);
+            if constexpr (kPair) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive_a(tempty_s + 8 * slot);
+            } else {
+              mbar_arrive_a(tempty_s + 8 * slot);
+            }
           }
         }
         const long long tl_d1 = tl_clock();
@@ -1184,16 +1293,23 @@ __global__ void __launch_bounds__(kSyrkThreads, 1) search_syrk_kernel(const DevD
     add_evals(s.evals, nevals);
   }
   fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync();  // the leader's last commits reached the peer
+  else __syncthreads();
   if (warp == 0) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
   }
 }
 
 inline uint64_t tiles_of(uint64_t M, uint64_t i) {
   const uint64_t nb = (M - 1 - i + kJB - 1) / kJB;
-  return nb * (nb + 1) / 2;
+  if (!kPair) return nb * (nb + 1) / 2;
+  uint64_t t = 0;  // pairs of j blocks: (nb - 2 p) k blocks each
+  for (uint64_t p = 0; p < n_jb(uint32_t(nb)); ++p) t += nb - 2 * p;
+  return t;
 }
 
 }  // namespace syrk
