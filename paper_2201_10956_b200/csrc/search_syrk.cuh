@@ -276,6 +276,10 @@ constexpr int kRoundUnroll = E3_ROUND_UNROLL;  // narrow epilogue: unroll of the
 #ifndef E3_MMA_WARP
 #define E3_MMA_WARP 1  // MMA issuer as a converged warp (elect inside the asm)
 #endif
+#ifndef E3_PROD_DEPTH
+#define E3_PROD_DEPTH 3  // producers: operand stages of Y words in flight (2 or 3 register sets;
+                         // 3: cfg4 371 -> 405 Tel/s, its Y streams from HBM; 4 measured slower)
+#endif
 #ifndef E3_MMA_AC_UNROLL
 #define E3_MMA_AC_UNROLL 1
 #define E3_MMA_CH_UNROLL 1
@@ -766,11 +770,12 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
           const uint4* __restrict__ Yb = s.Y + inf.y_off[a] + row_b;
           const uint32_t R = inf.R;
           const uint32_t qtot = inf.q[a][0] + inf.q[a][1];  // even: 256-sample stages
-          // Y quads of the next two stages in flight (L2 latency): two
-          // register sets, the loop unrolled over stage pairs so the load of
-          // stage q + 2 goes into the set stage q just consumed (register
-          // rotation would wait for the in-flight loads one stage early), with
-          // running row pointers (no per-load 64-bit index arithmetic)
+          // Y quads of the next E3_PROD_DEPTH stages in flight (L2 / HBM
+          // latency): that many named register sets, the loop unrolled over
+          // them so the load of stage q + depth refills the set stage q just
+          // consumed (register rotation would wait for the in-flight loads one
+          // stage early; indexed register arrays compiled badly), with running
+          // row pointers (no per-load 64-bit index arithmetic)
           const uint32_t nsu = qtot / 2;  // stages of this unit
           const size_t R2 = size_t(2) * R;
           uint4 a00, a01, b00, b01, a10, a11, b10, b11;
@@ -803,6 +808,25 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
             if (lane == 0) mbar_arrive_a(full_s + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1; }
           };
+#if E3_PROD_DEPTH == 3
+          // three register sets: the load of stage q + 3 refills the set stage q used
+          uint4 a20, a21, b20, b21;
+          if (nsu > 0) load(a00, a01, b00, b01);
+          if (nsu > 1) load(a10, a11, b10, b11);
+          if (nsu > 2) load(a20, a21, b20, b21);
+          for (uint32_t u3 = 0; u3 < nsu; u3 += 3) {
+            stage(a00, a01, b00, b01);
+            if (u3 + 3 < nsu) load(a00, a01, b00, b01);
+            if (u3 + 1 < nsu) {
+              stage(a10, a11, b10, b11);
+              if (u3 + 4 < nsu) load(a10, a11, b10, b11);
+            }
+            if (u3 + 2 < nsu) {
+              stage(a20, a21, b20, b21);
+              if (u3 + 5 < nsu) load(a20, a21, b20, b21);
+            }
+          }
+#else
           if (nsu > 0) load(a00, a01, b00, b01);
           if (nsu > 1) load(a10, a11, b10, b11);
           for (uint32_t u2 = 0; u2 < nsu; u2 += 2) {
@@ -813,6 +837,7 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
               if (u2 + 3 < nsu) load(a10, a11, b10, b11);
             }
           }
+#endif
         }
         wk.next(s);
       }
