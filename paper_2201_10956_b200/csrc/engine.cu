@@ -1566,7 +1566,9 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
   if (ymax > ds->y_cap) {
     dfree(ds, ds->y_buf);
     ds->y_buf = nullptr;
-    CUDA_TRY(dmalloc(ds, &ds->y_buf, 2 * sizeof(uint4) * std::max<size_t>(ymax, 1)));
+    // + 256 uint4: the Y staging ring's bulk copies read whole 128-row blocks,
+    // up to 127 rows past a quad's end (garbage rows of invalid triples)
+    CUDA_TRY(dmalloc(ds, &ds->y_buf, 2 * sizeof(uint4) * std::max<size_t>(ymax, 1) + 256 * sizeof(uint4)));
     ds->y_cap = ymax;
   }
   // the two metadata buffers are sized independently: a later search may need
@@ -1632,6 +1634,16 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
       }
     }
   }
+  // Y staging ring in the shared memory left over (>= 4 slots, else the
+  // producers prefetch into registers); E3_NO_YRING=1 disables it
+  uint32_t ny = 0;
+  if (!syrk::kPair && !std::getenv("E3_NO_YRING")) {
+    const size_t lim = sscr ? ds->smem_ss_cap : cap;
+    const size_t have = lim > tsm + 256 ? lim - tsm - 256 : 0;
+    ny = uint32_t(std::min<size_t>(syrk::kMaxYSlots, have / syrk::kYSlotBytes));
+    if (ny < 4) ny = 0;
+    else tsm += 256 + size_t(ny) * syrk::kYSlotBytes;
+  }
   // compaction waits for the metadata upload (and all earlier work on st)
   CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_upload, 0));
   for (size_t b = 0; b < batches.size(); ++b) {
@@ -1659,6 +1671,7 @@ int run_syrk(e3_dataset* ds, const DevData& d, uint64_t r0, uint64_t r1, uint32_
     sa.screen = screen ? 1u : 0u;
     sa.nst = nst;
     sa.ktab_n = ktab_use;
+    sa.ny = ny;
     // batch b's compaction overlaps batch b-1's search; it may reuse buffer
     // b & 1 only once batch b-2's search is done with it
     if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(ds->cstream, ds->ev_sdone[buf], 0));

@@ -256,6 +256,13 @@ __device__ __forceinline__ uint2 lds_u64(uint32_t a) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
   return v;
 }
+// Y staging ring (when shared memory is free: no screening table / global
+// scratch, e.g. cfg4): warp 13 streams each operand stage's bit-packed Y rows
+// (A quads q, q+1 and B quads q, q+1: four 2 KiB bulk copies, 128 rows x 16 B
+// each, contiguous in the quad-major Y layout) into a slot ahead of the
+// producers, who then read their row with one conflict-free LDS.128 each.
+constexpr int kMaxYSlots = 16;
+constexpr int kYSlotBytes = 4 * 128 * 16;
 constexpr int kSyrkProducerWarps = 4;
 constexpr int kSyrkThreads = 32 * 16;
 #ifndef E3_REG_PROD
@@ -325,6 +332,7 @@ struct SyrkArgs {
   uint32_t screen;                   // 1: K2 screening table in shared memory (d.ktab)
   uint32_t nst;                      // operand stages in use (2..kSyrkStages)
   uint32_t ktab_n;                   // screening-table entries staged in shared memory
+  uint32_t ny;                       // Y staging slots in shared memory (0: register prefetch)
 };
 
 // Profiling-only variants (E3_DEBUG_SKIP) exist only in a library built with
@@ -594,6 +602,9 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
   float* ktab = reinterpret_cast<float*>(lists + size_t(kEpilogueWarps) * 2 * s.top_k);
   // narrow: per-warp k staging (kKStageTotal bytes) after the screening table
   uint8_t* kstage = reinterpret_cast<uint8_t*>(ktab) + (s.screen ? size_t(s.ktab_n) * 4 : 0);
+  uint8_t* yring = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(kstage + (kNarrow ? kKStageTotal : 0)) + 127) & ~uintptr_t(127));
+  __shared__ uint64_t yfull_bar[kMaxYSlots], yempty_bar[kMaxYSlots];
   __shared__ uint64_t full_bar[kSyrkStages], empty_bar[kSyrkStages];
   __shared__ uint64_t tfull_bar[kUnits], tempty_bar[kUnits];
   __shared__ uint32_t tmem_base_sh;
@@ -613,6 +624,10 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
       // kPair: the leader's barriers also count one forwarded arrival from the peer
       mbar_init(&full_bar[st], kSyrkProducerWarps + (kPair && crank == 0 ? 1 : 0));
       mbar_init(&empty_bar[st], 1);
+    }
+    for (uint32_t y = 0; y < s.ny; ++y) {
+      mbar_init(&yfull_bar[y], 1);
+      mbar_init(&yempty_bar[y], kSyrkProducerWarps);
     }
     for (int b = 0; b < kUnits; ++b) {
       mbar_init(&tfull_bar[b], 1);
@@ -753,7 +768,46 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
     const uint32_t stage_b = smem_u32(stages) + row_off;
     const uint32_t tmem_a = tmem + (uint32_t((warp & 3) * 32) << 16) + kACol;
     const bool has_b = !kPair || r < 64;        // kPair: each CTA expands 64 B rows (warp-uniform)
-    if (it0 < it1) {
+    if (it0 < it1 && s.ny > 0) {
+      // Y words from the staging ring (warp 13 streams them ahead)
+      SWalker wk;
+      wk.start(s, it0);
+      uint32_t st = 0, ph = 0, ys = 0, yph = 0;
+      const uint32_t ring_s = smem_u32(yring) + r * 16;
+      const uint32_t yfull_s = smem_u32(yfull_bar), yempty_s = smem_u32(yempty_bar);
+      for (uint64_t it = it0; it < it1; ++it) {
+        const IInfo inf = s.info[wk.ii];
+#pragma unroll 1
+        for (uint32_t a = 0; a < 2; ++a) {
+          const uint32_t nsu = (inf.q[a][0] + inf.q[a][1]) / 2;
+          for (uint32_t u = 0; u < nsu; ++u) {
+            mbar_wait_a(yfull_s + 8 * ys, yph);
+            const uint32_t yb = ring_s + ys * kYSlotBytes;
+            const uint4 x0 = lds_u128(yb), x1 = lds_u128(yb + 2048);
+            const uint4 y0 = lds_u128(yb + 4096), y1 = lds_u128(yb + 6144);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(yempty_s + 8 * ys);
+            if (++ys == s.ny) { ys = 0; yph ^= 1; }
+            mbar_wait_a(empty_s + 8 * st, ph ^ 1);
+            fence_after();  // the MMAs that read this stage have completed
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t av[16];
+              expand_stage_regs(av, x0, x1, hf);
+              tmem_st16(tmem_a + st * kAStageCols + 16 * hf, av);
+            }
+            expand_stage_f4(stage_b + st * kSBStageBytes, y0, y1);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            fence_before();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(full_s + 8 * st);
+            if (++st == nst) { st = 0; ph ^= 1; }
+          }
+        }
+        wk.next(s);
+      }
+    } else if (it0 < it1) {
       SWalker wk;
       wk.start(s, it0);
       uint32_t st = 0, ph = 0;
@@ -845,6 +899,44 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
         printf("TL cta %d producer warp %d: total %lld wait_empty %lld\n", blockIdx.x, warp,
                tl_clock() - tl_t0, tl_w);
     }
+  } else if (warp == kMmaWarp + 1) {
+    // ===================== Y loader (staging ring, one thread) =====================
+    if (!kPair && s.ny > 0 && lane == 0 && it0 < it1) {
+      SWalker wk;
+      wk.start(s, it0);
+      uint32_t ys = 0, yph = 0;
+      const uint32_t ring = smem_u32(yring);
+      const uint32_t yfull_s = smem_u32(yfull_bar), yempty_s = smem_u32(yempty_bar);
+      for (uint64_t it = it0; it < it1; ++it) {
+        const IInfo inf = s.info[wk.ii];
+        const uint32_t R = inf.R;
+#pragma unroll 1
+        for (uint32_t a = 0; a < 2; ++a) {
+          // rows [128 jb, +128) and [128 kb, +128) of quads 2u, 2u + 1 (rows past
+          // R are garbage of the next quad: they only feed invalid triples)
+          const uint4* pa = s.Y + inf.y_off[a] + size_t(wk.jb) * 2 * kJB;
+          const uint4* pb = s.Y + inf.y_off[a] + size_t(wk.kb) * 2 * kJB;
+          const uint32_t nsu = (inf.q[a][0] + inf.q[a][1]) / 2;
+          for (uint32_t u = 0; u < nsu; ++u) {
+            mbar_wait_a(yempty_s + 8 * ys, yph ^ 1);
+            const uint32_t bar = yfull_s + 8 * ys, dst = ring + ys * kYSlotBytes;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                         "r"(uint32_t(kYSlotBytes)) : "memory");
+            const uint4* src[4] = {pa, pa + R, pb, pb + R};
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                  ::"r"(dst + x * 2048), "l"(src[x]), "r"(2048u), "r"(bar) : "memory");
+            pa += size_t(2) * R;
+            pb += size_t(2) * R;
+            if (++ys == s.ny) { ys = 0; yph ^= 1; }
+          }
+        }
+        wk.next(s);
+      }
+    }
+    __syncwarp();
   } else if (warp < kMmaWarp) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpilogue));
     // ===================== epilogue =====================
