@@ -1,2 +1,4 @@
-timeout 1200 python -m pytest tests -q -m gpu 2>&1 | tail -2
-E3_LIBCU=build/v_tl7/libepi3cu.so timeout 300 python tools/syrk_time.py --workload cfg4 --lo 0.25 --hi 0.27 --reps 1 > gpurun_out/tl_cfg4c.txt 2>&1
+for rep in 1 2; do
+E3_LIBCU=build/v_g/libepi3cu.so timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('r02g-build', round(d['value'],2))"
+timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('current', round(d['value'],2))"
+done
