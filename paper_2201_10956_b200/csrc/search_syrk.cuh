@@ -284,8 +284,8 @@ constexpr int kRoundUnroll = E3_ROUND_UNROLL;  // narrow epilogue: unroll of the
 #define E3_MMA_WARP 1  // MMA issuer as a converged warp (elect inside the asm)
 #endif
 #ifndef E3_PROD_DEPTH
-#define E3_PROD_DEPTH 3  // producers: operand stages of Y words in flight (2 or 3 register sets;
-                         // 3: cfg4 371 -> 405 Tel/s, its Y streams from HBM; 4 measured slower)
+#define E3_PROD_DEPTH 0  // producers: operand stages of Y words in flight (2 or 3 register sets;
+                         // 0 = per kernel mode, see kProdDepth; 4 measured slower)
 #endif
 #ifndef E3_MMA_AC_UNROLL
 #define E3_MMA_AC_UNROLL 1
@@ -590,6 +590,10 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
   constexpr bool kNarrow = kMode >= 1;
   static_assert(kNarrow || !kSS, "shared-memory scratch is narrow-only");
   constexpr uint32_t kSh = kMode >= 2 ? 2u : 0u;  // count scale shift of packed words
+  // producer prefetch depth: 3 where the operands stream (cfg4 +9%, cfg5 +1.3%,
+  // cfg2 +1.5%); 2 for the Stirling-scaled path (cfg3), where the larger loop
+  // cost 0.3% on the same box
+  constexpr int kProdDepth = E3_PROD_DEPTH == 0 ? (kMode == 3 ? 2 : 3) : E3_PROD_DEPTH;
   // no-swizzle K-major operand tiles need 16-byte alignment only
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
@@ -862,7 +866,7 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
             if (lane == 0) mbar_arrive_a(full_s + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1; }
           };
-#if E3_PROD_DEPTH == 3
+          if constexpr (kProdDepth == 3) {
           // three register sets: the load of stage q + 3 refills the set stage q used
           uint4 a20, a21, b20, b21;
           if (nsu > 0) load(a00, a01, b00, b01);
@@ -880,7 +884,7 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
               if (u3 + 5 < nsu) load(a20, a21, b20, b21);
             }
           }
-#else
+          } else {
           if (nsu > 0) load(a00, a01, b00, b01);
           if (nsu > 1) load(a10, a11, b10, b11);
           for (uint32_t u2 = 0; u2 < nsu; u2 += 2) {
@@ -891,7 +895,7 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
               if (u2 + 3 < nsu) load(a10, a11, b10, b11);
             }
           }
-#endif
+          }
         }
         wk.next(s);
       }
