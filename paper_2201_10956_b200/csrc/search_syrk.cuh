@@ -789,6 +789,10 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
             const uint32_t yb = ring_s + ys * kYSlotBytes;
             const uint4 x0 = lds_u128(yb), x1 = lds_u128(yb + 2048);
             const uint4 y0 = lds_u128(yb + 4096), y1 = lds_u128(yb + 6144);
+            // generic-proxy reads of the slot before the loader's next bulk copy
+            // (async proxy) overwrites it: without this proxy fence the copy
+            // could land first (cfg4: 4 of 150 searches differed)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive_a(yempty_s + 8 * ys);
             if (++ys == s.ny) { ys = 0; yph ^= 1; }

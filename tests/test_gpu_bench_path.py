@@ -194,3 +194,24 @@ def test_large_m_fits_or_fails_cleanly():
                                np.zeros((150_000, 2, 1), dtype=np.uint64))
     with pytest.raises(epi3.DeviceError, match="needs .* GB of device memory"):
         epi3.DeviceDataset(big)
+
+
+@pytest.mark.gpu
+def test_y_staging_ring_repeats_identically():
+    """A wide, long-sample dataset (no screening table: the shared memory goes
+    to the Y staging ring) searched 60 times on one resident dataset returns
+    the identical outcome every time; a missing generic->async proxy fence
+    in the ring once let 3% of cfg4 searches read a half-overwritten slot."""
+    import os
+    assert "E3_NO_YRING" not in os.environ
+    geno, pheno = epi3.generate_synthetic(260, 140_000, 0.3, 77,
+                                          epi3.PlantSpec((3, 100, 250), (1, 1, 1), 0.9, 0.3),
+                                          exact_cases=70_000)
+    ds = epi3.binarize(geno, pheno)
+    od = po.OracleDataset.of(ds)
+    with epi3.DeviceDataset(ds) as dd:
+        first = dd.search(epi3.SearchConfig(top_k=10))
+        for h in first.top:
+            assert od.score(h.triple).hex() == h.score.hex(), h
+        for _ in range(60):
+            assert epi3.same_outcome(first, dd.search(epi3.SearchConfig(top_k=10)))

@@ -1,4 +1,4 @@
 for rep in 1 2; do
-for n in d3all dmode; do
-E3_LIBCU=build/v_$n/libepi3cu.so timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$n', round(d['value'],2))"
-done; done
+timeout 600 python bench.py --workload cfg4 --steps 5 --warmup 3 --no-cpu --no-e2e > /tmp/o.json 2> /tmp/o.err; echo "ring+fence rc=$? $(python -c "import json; d=json.loads(open('/tmp/o.json').read().strip().splitlines()[-1]); print(round(d['value'],1))")"
+E3_NO_YRING=1 timeout 600 python bench.py --workload cfg4 --steps 5 --warmup 3 --no-cpu --no-e2e > /tmp/o.json 2> /tmp/o.err; echo "noring rc=$? $(python -c "import json; d=json.loads(open('/tmp/o.json').read().strip().splitlines()[-1]); print(round(d['value'],1))")"
+done
