@@ -1,3 +1,4 @@
-timeout 600 python tools/repeat_check.py cfg3 30 2>&1 | tail -2
-timeout 600 python tools/repeat_check.py cfg5 100 2>&1 | tail -2
-timeout 600 python tools/repeat_check.py cfg2 300 2>&1 | tail -2
+timeout 900 python tools/repeat_create_check.py cfg2 60 2>&1 | tail -2
+timeout 900 python tools/repeat_create_check.py cfg2 20 tc_masked 2>&1 | tail -2
+timeout 900 python tools/repeat_create_check.py cfg1 100 2>&1 | tail -2
+timeout 900 python tools/repeat_create_check.py cfg4 15 2>&1 | tail -2
