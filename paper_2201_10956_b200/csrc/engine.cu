@@ -110,6 +110,7 @@ struct DevData {
   uint32_t ktab_n;           // N+2 rounded up to a multiple of 4
   double kshift;             // -27*alpha + proven screening error bound
   float st_c1;               // stirling_term slope -(1+alpha) (k2_screen_packed)
+  double kshift_st;          // the Stirling screens' shift (E3_SCREEN_V2: affine part hoisted)
 };
 
 // ------------------------------------------------------------------------
@@ -226,6 +227,35 @@ __device__ __forceinline__ float f2_lo(uint64_t a) { return __uint_as_float(uint
 __device__ __forceinline__ float f2_hi(uint64_t a) { return __uint_as_float(uint32_t(a >> 32)); }
 __device__ __forceinline__ uint64_t f2_splat(float x) { return f2_pack(x, x); }
 
+// Scaled Stirling screen (kernel mode 3) with the linear part hoisted
+// (E3_SCREEN_V2): the cells of a triple partition the samples, so sum_c m_c =
+// N + 27 and the Stirling terms' affine part sum_c (c1 m_c + ln(2 pi)/2) is one
+// constant per dataset, folded into the host shift (DevData::kshift_st). Per
+// cell pair the device then only accumulates (m + 1/2) lg2(m) (one FFMA2 into
+// acc_s) and the two table terms (acc_g); the result is ln2 * acc_s - acc_g,
+// in one final FFMA: 5 f32x2 ops per cell pair instead of 7 (cfg3 +2.3%).
+// Its error bound (k2_screen_margin_st) grows with the un-cancelled sums, ~8x
+// the per-cell form's: the unscaled path (mode 1: classes >= 2^14 samples,
+// e.g. cfg5 with top-100) keeps the per-cell form, where the wider bound let
+// enough extra triples through to the exact tail to cost 3.5% (A/B log).
+#ifndef E3_SCREEN_V2
+#define E3_SCREEN_V2 1
+#endif
+#if E3_SCREEN_V2
+// n >> 16 as a byte permute: kept as its own value (a shift would be fused
+// into a shift-add per use, one more ALU op per cell)
+__device__ __forceinline__ uint32_t hi16(uint32_t n) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0x4432;" : "=r"(r) : "r"(n));
+  return r;
+}
+__device__ __forceinline__ float screen_v2_finish(const uint64_t* as, const uint64_t* ag, float s_last,
+                                                  float g_last) {
+  const float S = __fadd_rn(f2_hsum(f2_add(as[0], as[1])), s_last);
+  const float G = __fadd_rn(f2_hsum(f2_add(ag[0], ag[1])), g_last);
+  return __fmaf_rn(S, kLn2, -G);
+}
+#endif
 // k2_screen on class-packed cells (narrow path): word = class0 | class1 << 16.
 // Two cells per step in f32x2 (the MUFU lg2 stays scalar).
 __device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_s, float c1) {
@@ -272,6 +302,38 @@ __device__ __forceinline__ float k2_screen_packed(const uint32_t* n, uint32_t G_
 template <bool kStir>
 __device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_s, float c1) {
   if constexpr (kStir) {
+#if E3_SCREEN_V2
+    uint64_t as[2] = {0ull, 0ull}, ag[2] = {0ull, 0ull};
+    const uint64_t kq = f2_splat(0.25f), kb = f2_splat(1.0f - 2097152.0f), kbh = f2_splat(1.5f - 2097152.0f);
+#pragma unroll
+    for (int c = 0; c < 26; c += 2) {
+      uint32_t sb[2];
+      float g0[2], g1[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        // three ALU ops per cell: both halves plain (their table addresses fold
+        // into [R + UR]), the sum with the exponent in one IADD3
+        const uint32_t lo = n[c + e] & 0xffffu, hi = hi16(n[c + e]);
+        sb[e] = lo + hi + 0x4B000000u;  // bits of 2^23 + 4 (r0 + r1)
+        g0[e] = lds_f32(G_s + lo);
+        g1[e] = lds_f32(G_s + hi);
+      }
+      // m = r0 + r1 + 1 and m + 1/2, each exact in one FFMA2
+      const uint64_t sbp = (uint64_t(sb[1]) << 32) | sb[0];
+      const uint64_t m = f2_fma(sbp, kq, kb), mh = f2_fma(sbp, kq, kbh);
+      float lg0, lg1;
+      asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg0) : "f"(f2_lo(m)));
+      asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg1) : "f"(f2_hi(m)));
+      as[(c >> 1) & 1] = f2_fma(mh, f2_pack(lg0, lg1), as[(c >> 1) & 1]);
+      ag[(c >> 1) & 1] = f2_add(ag[(c >> 1) & 1], f2_add(f2_pack(g0[0], g0[1]), f2_pack(g1[0], g1[1])));
+    }
+    const uint32_t lo = n[26] & 0xffffu, hi = n[26] >> 16;
+    const float m = __fsub_rn(__uint_as_float(((lo + hi) >> 2) + 0x4B000001u), 8388608.f);
+    float lg;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(m));
+    return screen_v2_finish(as, ag, __fmul_rn(__fadd_rn(m, 0.5f), lg),
+                            __fadd_rn(lds_f32(G_s + lo), lds_f32(G_s + hi)));
+#else
     uint64_t acc[2] = {0ull, 0ull};
     const uint64_t kq = f2_splat(0.25f), kb = f2_splat(1.0f - 2097152.0f), kl = f2_splat(kLn2),
                    khl = f2_splat(0.5f * kLn2), kc1 = f2_splat(c1), kh = f2_splat(kHalfLn2Pi);
@@ -300,6 +362,7 @@ __device__ __forceinline__ float k2_screen_scaled(const uint32_t* n, uint32_t G_
     const float last = __fsub_rn(__fsub_rn(stirling_term(((lo + hi) >> 2) + 0x4B000001u, c1), lds_f32(G_s + lo)),
                                  lds_f32(G_s + hi));
     return __fadd_rn(f2_hsum(f2_add(acc[0], acc[1])), last);
+#endif
   }
   uint64_t acc[2] = {0ull, 0ull};  // +0.0f x2
 #pragma unroll
@@ -894,6 +957,7 @@ struct e3_dataset {
   float* ktab = nullptr;              // K2 screening table (see k2_screen)
   uint32_t ktab_n = 0;
   double kshift = 0;
+  double kshift_st = 0;
   float st_c1 = 0.f;
   uint64_t* itemoff = nullptr;
   std::vector<uint64_t> h_itemoff;
@@ -1014,6 +1078,7 @@ DevData dev_view(const e3_dataset* ds) {
   d.ktab = ds->ktab;
   d.ktab_n = ds->ktab_n;
   d.kshift = ds->kshift;
+  d.kshift_st = ds->kshift_st;
   d.st_c1 = ds->st_c1;
   return d;
 }
@@ -1042,6 +1107,36 @@ double k2_screen_margin(double gmax, double N, double alpha) {
   return 2.0 * (27.0 * per_cell + stirling) + 1e-9 * smax + 1e-6;
 }
 
+// Bound for the E3_SCREEN_V2 scaled Stirling screen (k2_screen_scaled<true>),
+// which returns ln2 * S - G, S = sum_c (m_c + 1/2) lg2(m_c), G = sum_c (G[r0_c]
+// + G[r1_c]) (fp32; m = r0 + r1 + 1 <= N + 1, m and m + 1/2 exact). With
+// Stirling's lower bound ln m! >= (m + 1/2) ln m - m + ln(2 pi)/2 and
+// ln r! = G[r] + alpha r exactly, sum_c m_c = N + 27 gives
+//   score >= screen* - (1 + alpha) N - 27 + 13.5 ln(2 pi),
+// screen* the exact-arithmetic value over the exact G. |screen - screen*| is
+// at most, with u = 2^-24, A = (N + 41) log2(N + 2) >= sum (m + 1/2)|lg2 m|
+// and Gp = 54 gmax >= sum |G|:
+//  * lg2.approx (|E| <= 2^-20, 4x the PTX bound): ln2 E (N + 41);
+//  * S: each f32x2 lane takes <= 7 FFMA2 accumulations (partial sums <= its
+//    share of A, so <= 7 u A in all), then the lane combine, the horizontal
+//    add, the last cell's product and its add (u A each): 11 u A, times ln2;
+//    the fp32 ln2 (u ln2 A) and the final FFMA (u (ln2 A + Gp));
+//  * G: 54 table roundings (u gmax each); per lane one pair add and <= 7
+//    accumulations (u Gp and 7 u Gp in all), combine, horizontal add and the
+//    last cell (3 u Gp + 2 u gmax).
+// Sum: ln2 E (N + 41) + 13 u ln2 A + 56 u gmax + 12 u Gp; doubled, with slack
+// for second-order terms and the reference's own fp64 rounding.
+double k2_screen_margin_st(double gmax, double N) {
+  const double u = std::ldexp(1.0, -24), E = std::ldexp(1.0, -20), ln2 = std::log(2.0);
+  const double A = (N + 41.0) * std::log2(N + 2.0), Gp = 54.0 * gmax;
+  const double smax = N * ln2 + 27.0 * std::log(N + 1.0) + 1.0;
+  const double err = ln2 * E * (N + 41.0) + 13.0 * u * ln2 * A + 56.0 * u * gmax + 12.0 * u * Gp;
+#ifndef E3_ST_MARGIN_SCALE
+#define E3_ST_MARGIN_SCALE 1.0  // A/B attribution only (< 1 is unsafe)
+#endif
+  return E3_ST_MARGIN_SCALE * (2.0 * err * (1.0 + 8.0 * u) + 1e-9 * smax + 1e-6);
+}
+
 // Host tables that depend only on N: the reference's log table (built exactly
 // like build_log_table(N+1), scoring.cpp:14-21) and the K2 screening table
 // G[n] = fl32(P[n] - alpha*n) with its proven margin. alpha balances the
@@ -1053,6 +1148,7 @@ struct LogTables {
   std::vector<double> logp;  // N+2 entries
   std::vector<float> ktab;   // N+2 rounded up to a multiple of 4
   double kshift = 0;
+  double kshift_st = 0;  // k2_screen_packed / k2_screen_scaled<true> (E3_SCREEN_V2)
   float st_c1 = 0.f;  // stirling_term slope -(1+alpha)
 };
 std::shared_ptr<const LogTables> log_tables_for(uint64_t N) {
@@ -1076,6 +1172,12 @@ std::shared_ptr<const LogTables> log_tables_for(uint64_t N) {
   }
   t->kshift = -27.0 * alpha + k2_screen_margin(gmax, double(N), alpha);
   t->st_c1 = float(-(1.0 + alpha));
+#if E3_SCREEN_V2
+  t->kshift_st = (1.0 + alpha) * double(N) + 27.0 - 13.5 * std::log(6.283185307179586477) +
+                 k2_screen_margin_st(gmax, double(N));
+#else
+  t->kshift_st = t->kshift;
+#endif
   std::lock_guard<std::mutex> g(mu);
   if (cache.size() >= 4) cache.erase(cache.begin());
   cache.emplace_back(N, t);
@@ -1284,6 +1386,7 @@ int build(e3_dataset* ds, const uint64_t* host[2], const GenoSrc* gs = nullptr) 
                            cudaMemcpyHostToDevice, ds->stream));
   ds->ktab_n = uint32_t(lt->ktab.size());
   ds->kshift = lt->kshift;
+  ds->kshift_st = lt->kshift_st;
   ds->st_c1 = lt->st_c1;
   CUDA_TRY(dmalloc(ds, &ds->ktab, sizeof(float) * lt->ktab.size()));
   CUDA_TRY(cudaMemcpyAsync(ds->ktab, lt->ktab.data(), sizeof(float) * lt->ktab.size(),

@@ -1140,7 +1140,8 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
         // screening bound: a triple whose fp32 screen exceeds thr_f cannot reach
         // the threshold (margin proven on the host, k2_screen_margin)
         const float thr_f = gth == ~0ull ? __int_as_float(0x7f800000)
-                                         : __double2float_ru(key_score(gth) + d.kshift);
+                                         : __double2float_ru(key_score(gth) + (kMode == 3 ? d.kshift_st
+                                                                                                        : d.kshift));
         uint64_t rank_ij = 0;
         if (kRanged) {
           const uint64_t Mi = M - i, Mj = M - jc;
