@@ -273,6 +273,9 @@ constexpr int kSyrkThreads = 32 * 16;
 #define E3_REG_MMA 56
 #endif
 constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = E3_REG_MMA;
+#ifndef E3_W_INPLACE
+#define E3_W_INPLACE 1  // narrow rounds: next-round scratch words loaded in place after T
+#endif
 #ifndef E3_ROUND_UNROLL
 #define E3_ROUND_UNROLL 1
 #endif
@@ -1156,6 +1159,29 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
           const uint32_t mk2 = ~(mk0 | mk1);
           // the next round's pair(j,k) entries and scratch words are fetched one
           // round ahead (software pipelining across rounds)
+#if E3_W_INPLACE
+          // W[a][t][g]: this row (j, b=bsel), unit slot a, k phase t, genotype g;
+          // the next round's words are loaded into W itself once T is built
+          // (they land during the screen; no register copies)
+          uint32_t W[2][4][2];
+          auto load_w = [&](int mm) {
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+                  W[a][t][g] = scr_ld(a * kRounds * 8 + mm * 8 + t * 2 + g);
+          };
+          load_w(0);
+#pragma unroll kRoundUnroll
+          for (int m = 0; m < kRounds; ++m) {
+            uint4 pjk[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) pjk[h] = pjn[h];
+            if (m + 1 < kRounds) fetch_pairs(m + 1);
+            const int mnext = min(m + 1, kRounds - 1);
+#else
           uint32_t Wn[2][4][2];
           auto fetch_round = [&](int mm) {
             if (mm > 0) fetch_pairs(mm);
@@ -1182,6 +1208,7 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
 #pragma unroll
                 for (int g = 0; g < 2; ++g) W[a][t][g] = Wn[a][t][g];
             if (m + 1 < kRounds) fetch_round(m + 1);
+#endif
             // the partner row (j, b^1) sends its words for this thread's phases 2*bsel + h
             uint32_t rcv[2][2][2];
 #pragma unroll
@@ -1228,6 +1255,9 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
                     T[h][4 + b * 2 + g] = (s1 & mk2) | (X & mk1) | (s0 & mk0);
                   }
               }
+#if E3_W_INPLACE
+              load_w(mnext);
+#endif
               bool pass[2];
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
@@ -1276,6 +1306,11 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
                 lastT = r.lastT;
               }
             }
+#if E3_W_INPLACE
+            else {
+              load_w(mnext);
+            }
+#endif
           }
         } else {
           const uint4 pij0 = __ldg(d.pair[0] + size_t(i) * M + jc);

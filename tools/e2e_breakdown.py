@@ -14,7 +14,7 @@ from paper_2201_10956_b200 import epi3  # noqa: E402
 
 w = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-ds, desc, top_k = bench.make_dataset(w)
+ds, top_k, _ = bench.make_dataset(w)
 pin_c = torch.from_numpy(ds.ctrl.view("int64")).pin_memory()
 pin_k = torch.from_numpy(ds.cases.view("int64")).pin_memory()
 slices = epi3.partition(ds.num_snps, 64)
