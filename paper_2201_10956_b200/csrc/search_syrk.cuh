@@ -273,6 +273,9 @@ constexpr int kSyrkThreads = 32 * 16;
 #define E3_REG_MMA 56
 #endif
 constexpr int kRegProducer = E3_REG_PROD, kRegEpilogue = E3_REG_EPI, kRegMma = E3_REG_MMA;
+#ifndef E3_PJK_LATE
+#define E3_PJK_LATE 1  // mode 3 rounds (with E3_W_INPLACE): next pair(j,k) rows loaded after derive_cells
+#endif
 #ifndef E3_W_INPLACE
 #define E3_W_INPLACE 1  // narrow rounds: next-round scratch words loaded in place after T
 #endif
@@ -597,6 +600,8 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
   // cfg2 +1.5%); 2 for the Stirling-scaled path (cfg3), where the larger loop
   // cost 0.3% on the same box
   constexpr int kProdDepth = E3_PROD_DEPTH == 0 ? (kMode == 3 ? 2 : 3) : E3_PROD_DEPTH;
+  // measured: cfg3 (mode 3) +0.5%, cfg2 (mode 2) -1.6%
+  constexpr bool kPjkLate = E3_PJK_LATE && E3_W_INPLACE && kMode == 3;
   // no-swizzle K-major operand tiles need 16-byte alignment only
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
@@ -1176,10 +1181,17 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
           load_w(0);
 #pragma unroll kRoundUnroll
           for (int m = 0; m < kRounds; ++m) {
-            uint4 pjk[2];
+            // kPjkLate: this round's pair(j,k) rows are pjn itself, the next
+            // round's are loaded into it once derive_cells has used them
+            // (during the screens) and the rare tail reloads its own copy;
+            // otherwise they are copied and the next ones fetched here
+            uint4 pjk_copy[2];
+            if constexpr (!kPjkLate) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) pjk[h] = pjn[h];
-            if (m + 1 < kRounds) fetch_pairs(m + 1);
+              for (int h = 0; h < 2; ++h) pjk_copy[h] = pjn[h];
+              if (m + 1 < kRounds) fetch_pairs(m + 1);
+            }
+            uint4 (&pjk)[2] = kPjkLate ? pjn : pjk_copy;
             const int mnext = min(m + 1, kRounds - 1);
 #else
           uint32_t Wn[2][4][2];
@@ -1263,6 +1275,8 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
               for (int h = 0; h < 2; ++h) {
                 uint32_t n[27];
                 derive_cells(T[h], pij, pik[h], pjk[h], sip, sjp, skp[h], d.npk, n);
+                if constexpr (kPjkLate)
+                  if (m + 1 < kRounds) pjn[h] = __ldg(d.pairp + size_t(min(kbase + 4 * (m + 1) + h, M - 1)) * M + jc);
                 if (dbg_skip(s) & 2) {  // profiling: operands not expanded -> keep lookups in range
 #pragma unroll
                   for (int c = 0; c < 27; ++c) n[c] &= 0x0ffc0ffcu;
@@ -1288,7 +1302,7 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
 #pragma unroll
                   for (int x = 0; x < 8; ++x) in.T[h][x] = T[h][x];
                   in.pik[h] = pik[h];
-                  in.pjk[h] = pjk[h];
+                  in.pjk[h] = kPjkLate ? __ldg(d.pairp + size_t(min(kk[h], M - 1)) * M + jc) : pjk[h];
                   in.skp[h] = skp[h];
                   in.kk[h] = kk[h];
                   in.pass[h] = pass[h];
@@ -1309,6 +1323,8 @@ search_syrk_kernel(const DevData d, const SyrkArgs s) {
 #if E3_W_INPLACE
             else {
               load_w(mnext);
+              if constexpr (kPjkLate)
+                if (m + 1 < kRounds) fetch_pairs(m + 1);
             }
 #endif
           }
